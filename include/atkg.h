@@ -1,0 +1,234 @@
+/*
+ * atkg.h -- C ABI of the B200-native two-stage approximate top-k
+ * (arXiv 2506.04165), the drop-in boundary for the reference `atk` core.
+ *
+ * Every entry point replaces one reference interface (paths relative to
+ * /root/reference/proj/core):
+ *
+ *   atkg_validate                 AlgoParams::validate        include/atk/params.hpp:40, src/topk.cpp:54-67
+ *   atkg_validate_analysis        AlgoParams::validate_analysis  params.hpp:47, topk.cpp:69-76
+ *   atkg_stage1                   stage1_partial_reduce       include/atk/topk.hpp:98-99, src/topk.cpp:178-186
+ *   atkg_select_candidates        select_top_k_candidates     topk.hpp:109-112, topk.cpp:219-236
+ *   atkg_approx_top_k             approx_top_k / _batch       topk.hpp:117-124, topk.cpp:238-273
+ *   atkg_exact_top_k              exact_top_k                 topk.hpp:104, topk.cpp:206-217
+ *   atkg_measure_recall           measure_recall              topk.hpp:128, topk.cpp:275-297
+ *   atkg_stage1_summary /
+ *   atkg_summary_merge_top_k      Stage1Accumulator::consume over a slice of one
+ *                                 row + the cross-slice merge  topk.hpp:68-94, topk.cpp:123-172
+ *   atkg_accumulator_*            Stage1Accumulator           topk.hpp:68-94
+ *   atkg_exact_expected_recall    exact_expected_recall       include/atk/recall.hpp:39, src/recall.cpp:76-100
+ *   atkg_mc_expected_recall       mc_expected_recall          recall.hpp:45-46, recall.cpp:102-154
+ *   atkg_mc_expected_recall_adaptive  mc_expected_recall_adaptive  recall.hpp:50-51, recall.cpp:156-165
+ *   atkg_legal_bucket_counts      legal_bucket_counts         include/atk/planner.hpp:61-62, src/planner.cpp:59-77
+ *   atkg_select_parameters        select_parameters           planner.hpp:66-67, planner.cpp:79-147
+ *   atkg_fused_gemm_top_k         mips_fused semantics (stage 1 in the matmul epilogue)
+ *                                 include/atk/mips.hpp:50-52, src/mips.cpp:138-193
+ *
+ * Conventions
+ *   - Device entry points take DEVICE pointers and a cudaStream_t passed as
+ *     void*; they only enqueue work (no host synchronisation).  Outputs are
+ *     caller-owned.  Temporary storage is caller-supplied through `ws`
+ *     (size from atkg_workspace_size), so concurrent streams never share state.
+ *   - NaN detection is a device flag: kernels OR ATKG_FLAG_NAN into *d_status
+ *     (a caller-zeroed uint32 in device memory).  atkg_check_status()
+ *     synchronises the stream and maps the flags to ATKG_ENAN
+ *     ("input contains NaN", the reference's std::invalid_argument).
+ *   - *_host entry points are the drop-in form of the reference's span API:
+ *     host buffers in, host buffers out, synchronous, errors returned with
+ *     the reference's exact messages (atkg_last_error()).
+ *   - Indices are uint32 element positions in the source row, identical to
+ *     the reference's std::uint32_t (bit-identical to int32 for n < 2^31).
+ *   - Values are fp32.  bf16 inputs are upcast exactly.
+ */
+#ifndef ATKG_H_
+#define ATKG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; messages via atkg_last_error() (thread-local) */
+#define ATKG_OK 0
+#define ATKG_EINVAL 1         /* std::invalid_argument */
+#define ATKG_ENAN 2           /* std::invalid_argument("input contains NaN") */
+#define ATKG_EINFEASIBLE 3    /* atk::NoFeasibleConfigError */
+#define ATKG_ECUDA 4          /* CUDA runtime failure */
+#define ATKG_EUNSUPPORTED 5   /* shape outside what the device path implements */
+
+#define ATKG_FLAG_NAN 1u
+
+/* element types of the input rows */
+#define ATKG_F32 0
+#define ATKG_BF16 1
+
+/* operations for atkg_workspace_size */
+#define ATKG_OP_STAGE1 0
+#define ATKG_OP_APPROX 1
+#define ATKG_OP_SELECT 2
+#define ATKG_OP_EXACT 3
+#define ATKG_OP_SUMMARY 4
+#define ATKG_OP_MERGE 5
+
+/* AlgoParams (include/atk/params.hpp:20-48); lane_multiple default 128 */
+typedef struct atkg_params {
+  uint64_t n;
+  uint64_t num_buckets;
+  uint32_t local_k;
+  uint32_t global_k;
+  uint32_t lane_multiple;
+} atkg_params;
+
+const char* atkg_last_error(void);
+const char* atkg_version(void);
+
+int atkg_validate(const atkg_params* p);
+int atkg_validate_analysis(const atkg_params* p);
+
+/* ---- device entry points ------------------------------------------------ */
+
+/* Bytes of caller-supplied workspace needed by `op`.  For ATKG_OP_SELECT,
+ * p->n is the candidate count per row and p->global_k the k. For
+ * ATKG_OP_EXACT, p->n is the row length and p->global_k the k. */
+int atkg_workspace_size(int op, int dtype, uint64_t rows, const atkg_params* p,
+                        size_t* bytes);
+
+/* stage1_partial_reduce over `rows` contiguous rows of p->n elements:
+ * writes the bucket-minor grid [rows][local_k][num_buckets] (topk.hpp:59-67),
+ * bit-identical to the reference (Alg. 1 tie semantics, unfilled slots
+ * {-inf, 0}). */
+int atkg_stage1(int dtype, const void* d_in, uint64_t rows, const atkg_params* p,
+                float* d_grid_vals, uint32_t* d_grid_idx, void* d_ws, size_t ws_bytes,
+                uint32_t* d_status, void* stream);
+
+/* select_top_k_candidates per row: candidates row r live at
+ * d_vals[r*stride .. r*stride+count); indices >= index_limit are dropped;
+ * output [rows][k] sorted by (value desc, index asc), -0.0 emitted as +0.0.
+ * Rows with fewer than k surviving candidates raise ATKG_EINVAL
+ * ("fewer candidates than k") at atkg_check_status. */
+int atkg_select_candidates(const float* d_vals, const uint32_t* d_idx, uint64_t rows,
+                           uint64_t count, uint64_t stride, uint32_t k, uint64_t index_limit,
+                           float* d_out_vals, uint32_t* d_out_idx, void* d_ws, size_t ws_bytes,
+                           uint32_t* d_status, void* stream);
+
+/* approx_top_k_batch: stage 1 + stage 2 per row -> [rows][global_k]. */
+int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_params* p,
+                      float* d_out_vals, uint32_t* d_out_idx, void* d_ws, size_t ws_bytes,
+                      uint32_t* d_status, void* stream);
+
+/* exact_top_k per row (recall measurement only). */
+int atkg_exact_top_k(int dtype, const void* d_in, uint64_t rows, uint64_t n, uint32_t k,
+                     float* d_out_vals, uint32_t* d_out_idx, void* d_ws, size_t ws_bytes,
+                     uint32_t* d_status, void* stream);
+
+/* Slice summaries for sharding one row (or streaming it in blocks).
+ * The slice holds elements [index_offset, index_offset + len) of a row of
+ * p->n elements; index_offset and len are multiples of num_buckets.
+ * The summary of every bucket (ATKG_SUMMARY_WORDS(p) uint32 words) is exact
+ * and associative: atkg_summary_merge_top_k over the G slices' summaries,
+ * in index order, reproduces the reference stage-1 grid and its top-k
+ * bit-for-bit.  This is what crosses NVLink in the sharded giant-row path. */
+#define ATKG_SUMMARY_WORDS(p) ((2ull * (p)->local_k + 2ull) * (p)->num_buckets)
+int atkg_stage1_summary(int dtype, const void* d_slice, uint64_t len, uint64_t index_offset,
+                        const atkg_params* p, uint32_t* d_summary, void* d_ws, size_t ws_bytes,
+                        uint32_t* d_status, void* stream);
+/* Merges `parts` consecutive summaries (each ATKG_SUMMARY_WORDS words, in
+ * index order).  Writes the Alg. 1 grid if d_grid_vals != NULL, and the
+ * top-global_k if d_out_vals != NULL. */
+int atkg_summary_merge_top_k(const uint32_t* d_summaries, uint32_t parts, const atkg_params* p,
+                             float* d_grid_vals, uint32_t* d_grid_idx, float* d_out_vals,
+                             uint32_t* d_out_idx, void* d_ws, size_t ws_bytes,
+                             uint32_t* d_status, void* stream);
+
+/* Synchronises `stream`, reads *d_status and maps the flags to a status
+ * code (ATKG_ENAN / ATKG_EINVAL with the reference message). */
+int atkg_check_status(const uint32_t* d_status, void* stream);
+
+/* ---- streaming accumulator (Stage1Accumulator, topk.hpp:68-94) ---------- */
+typedef struct atkg_accumulator atkg_accumulator;
+int atkg_accumulator_create(const atkg_params* p, atkg_accumulator** out);
+/* consume the next `len` elements (positions consumed()..+len-1) of the row
+ * from device memory; any length, any alignment; stream-ordered */
+int atkg_accumulator_consume(atkg_accumulator* acc, int dtype, const void* d_block,
+                             uint64_t len, void* stream);
+uint64_t atkg_accumulator_consumed(const atkg_accumulator* acc);
+/* grid [local_k][num_buckets] (device pointers), synchronises */
+int atkg_accumulator_candidates(atkg_accumulator* acc, float* d_vals, uint32_t* d_idx,
+                                void* stream);
+void atkg_accumulator_destroy(atkg_accumulator* acc);
+
+/* ---- fused GEMM + stage 1 (C4: x[M,Kd] . W[Kd,N] -> top-k per row) ------ */
+/* x bf16 row-major [M][Kd]; w_t bf16 row-major [N][Kd] (W transposed, i.e.
+ * the MIPS "database" layout, mips.hpp:37-62).  Scores are fp32 accumulated
+ * on tcgen05 tensor cores; stage 1 runs in the epilogue.  Optionally writes
+ * the fp32 score matrix (d_scores != NULL, [M][N]) for oracle replay. */
+int atkg_fused_gemm_top_k(const void* d_x, const void* d_w_t, uint64_t m, uint64_t kdim,
+                          const atkg_params* p, float* d_out_vals, uint32_t* d_out_idx,
+                          float* d_scores, void* d_ws, size_t ws_bytes, uint32_t* d_status,
+                          void* stream);
+int atkg_fused_workspace_size(uint64_t m, uint64_t kdim, const atkg_params* p, size_t* bytes);
+/* plain tcgen05 bf16 GEMM, fp32 out (the unfused reference path) */
+int atkg_gemm_bf16(const void* d_x, const void* d_w_t, uint64_t m, uint64_t kdim, uint64_t n,
+                   float* d_out, void* stream);
+
+/* ---- host-buffer drop-in entry points (synchronous) --------------------- */
+int atkg_stage1_host(const float* in, uint64_t rows, const atkg_params* p, float* grid_vals,
+                     uint32_t* grid_idx);
+int atkg_select_candidates_host(const float* vals, const uint32_t* idx, uint64_t count,
+                                uint32_t k, uint64_t index_limit, float* out_vals,
+                                uint32_t* out_idx);
+int atkg_approx_top_k_host(const float* rows_in, uint64_t rows, const atkg_params* p,
+                           float* out_vals, uint32_t* out_idx);
+int atkg_exact_top_k_host(const float* in, uint64_t n, uint32_t k, float* out_vals,
+                          uint32_t* out_idx);
+
+/* ---- host analysis / planner -------------------------------------------- */
+int atkg_measure_recall(const uint32_t* approx_idx, uint64_t approx_k, const uint32_t* exact_idx,
+                        uint64_t exact_k, double* out);
+int atkg_exact_expected_recall(const atkg_params* p, double* out);
+int atkg_mc_expected_recall(const atkg_params* p, uint64_t trials, uint64_t seed, double* mean,
+                            double* std_error);
+int atkg_mc_expected_recall_adaptive(const atkg_params* p, uint64_t seed, double* mean,
+                                     double* std_error, uint64_t* trials);
+uint64_t atkg_legal_bucket_counts(uint64_t n, uint64_t lane_multiple, uint64_t* out,
+                                  uint64_t cap);
+
+/* PlanRequest / PlanResult (planner.hpp:18-39) */
+typedef struct atkg_plan_request {
+  uint64_t n;
+  uint64_t k;
+  double recall_target;
+  const uint32_t* allowed_local_k;
+  uint32_t num_allowed_local_k;
+  uint32_t lane_multiple;
+  uint64_t seed;
+} atkg_plan_request;
+#define ATKG_RECALL_EXACT 0
+#define ATKG_RECALL_MONTE_CARLO 1
+typedef struct atkg_plan_result {
+  uint32_t local_k;
+  uint64_t num_buckets;
+  uint64_t num_elements;
+  double recall;
+  int recall_method;       /* ATKG_RECALL_* */
+  double recall_std_error; /* monte_carlo only, else 0 */
+  uint64_t recall_trials;  /* monte_carlo only, else 0 */
+  int high_target_warning;
+} atkg_plan_result;
+int atkg_select_parameters(const atkg_plan_request* req, atkg_plan_result* out);
+
+/* ---- seeded synthetic inputs (documented convention) --------- */
+/* out[i] = mean + stddev * z_i, z from Box-Muller over xoshiro256++ streams
+ * derive_seed(seed, i / 65536) (rng.hpp:25-81), fp32. */
+void atkg_fill_normal(uint64_t seed, uint64_t count, float mean, float stddev, float* out,
+                      uint32_t threads);
+/* round-to-nearest-even fp32 -> bf16 bits */
+void atkg_f32_to_bf16(const float* in, uint64_t count, uint16_t* out, uint32_t threads);
+void atkg_bf16_to_f32(const uint16_t* in, uint64_t count, float* out, uint32_t threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATKG_H_ */

@@ -1,0 +1,781 @@
+// atkg_api.cu -- the C ABI (include/atkg.h): validation, workspace planning,
+// kernel dispatch, host-buffer drop-in entry points and the streaming
+// accumulator.  Kernels live in stage1.cuh / stage2.cuh / radix.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/atkg.h"
+#include "host_common.hpp"
+#include "radix.cuh"
+#include "stage1.cuh"
+#include "stage2.cuh"
+
+namespace atkg {
+
+thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+#define CUDA_OK(x)                                                                      \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+inline void check_launch() { CUDA_OK(cudaGetLastError()); }
+
+constexpr int kSegWarps = 8;   // warps (= segments) per stage-1 CTA
+constexpr int kPrefetch = 4;   // stride-rows per batch in the stage-1 loop
+constexpr uint32_t kMaxSortKeys = 16384;  // one CTA's shared-memory sort (128 KB)
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, c = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    return c > 0 ? c : 148;
+  }();
+  return n;
+}
+
+uint64_t align_up(uint64_t x, uint64_t a = 256) { return (x + a - 1) / a * a; }
+
+uint32_t next_pow2(uint64_t x) {
+  uint32_t p = 2;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+void validate(const atkg_params& p) {  // src/topk.cpp:54-67, same messages
+  if (p.n == 0) throw_inval("n must be >= 1");
+  if (p.n > 0xffffffffull) throw_inval("n exceeds the 32-bit index range");
+  if (p.num_buckets == 0) throw_inval("num_buckets must be >= 1");
+  if (p.n % p.num_buckets != 0) throw_inval("num_buckets must divide n");
+  if (p.lane_multiple == 0) throw_inval("lane_multiple must be >= 1");
+  if (p.num_buckets % p.lane_multiple != 0) throw_inval("num_buckets must be a multiple of lane_multiple");
+  if (p.local_k == 0) throw_inval("local_k must be >= 1");
+  if (p.global_k == 0) throw_inval("global_k must be >= 1");
+  if (p.global_k > p.n) throw_inval("global_k must not exceed n");
+  if (p.num_buckets * static_cast<uint64_t>(p.local_k) < p.global_k)
+    throw_inval("num_buckets * local_k must be >= global_k");
+}
+
+bool kp_specialised(uint32_t kp) { return (kp >= 1 && kp <= 8) || kp == 16; }
+
+// ---------------------------------------------------------------------------
+// stage-1 launch plan
+// ---------------------------------------------------------------------------
+struct S1Plan {
+  bool generic = false;
+  int V = 4;
+  uint32_t tiles = 0, segs = 0, cpr = 0;
+  uint64_t seg_len = 0, nstr = 0;
+  size_t smem = 0;
+  uint64_t summary_words() const { return 0; }
+};
+
+S1Plan plan_stage1(int dtype, const void* in, uint64_t rows, uint64_t len, uint64_t row_stride,
+                   uint64_t B, uint32_t kp) {
+  S1Plan pl;
+  const int esz = dtype == ATKG_BF16 ? 2 : 4;
+  const int V = 4;
+  const bool aligned = (reinterpret_cast<uintptr_t>(in) % (V * esz) == 0) && (row_stride % V == 0);
+  if (!kp_specialised(kp) || B % V != 0 || !aligned) {
+    pl.generic = true;
+    return pl;
+  }
+  pl.V = V;
+  pl.nstr = len / B;
+  pl.tiles = static_cast<uint32_t>(ceil_div(B, 32ull * V));
+  const uint64_t units = rows * pl.tiles;
+  const uint64_t target_warps = static_cast<uint64_t>(sm_count()) * 32;
+  const uint64_t min_len = std::max<uint64_t>(kp, 32);
+  uint64_t max_segs = std::max<uint64_t>(1, pl.nstr / min_len);
+  uint64_t segs = std::min<uint64_t>(max_segs, std::max<uint64_t>(1, ceil_div(target_warps, units)));
+  pl.seg_len = std::max<uint64_t>(1, ceil_div(pl.nstr, segs));
+  if (pl.nstr >= kp) pl.seg_len = std::max<uint64_t>(pl.seg_len, kp);
+  pl.segs = static_cast<uint32_t>(std::max<uint64_t>(1, ceil_div(pl.nstr, pl.seg_len)));
+  pl.cpr = static_cast<uint32_t>(ceil_div(pl.segs, kSegWarps));
+  pl.smem = static_cast<size_t>(kSegWarps / 2) * (2 * kp + 2) * V * 32 * 4;
+  return pl;
+}
+
+template <typename T, int KP>
+void launch_segments(const S1Plan& pl, const SegArgs& a, cudaStream_t st) {
+  auto kern = stage1_segments_kernel<T, KP, 4, kSegWarps, kPrefetch>;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    attr = true;
+  }
+  const uint64_t grid = a.rows * pl.tiles * pl.cpr;
+  kern<<<static_cast<unsigned>(grid), kSegWarps * 32, pl.smem, st>>>(a);
+  check_launch();
+}
+
+template <typename T>
+void dispatch_segments(uint32_t kp, const S1Plan& pl, const SegArgs& a, cudaStream_t st) {
+  switch (kp) {
+    case 1: launch_segments<T, 1>(pl, a, st); break;
+    case 2: launch_segments<T, 2>(pl, a, st); break;
+    case 3: launch_segments<T, 3>(pl, a, st); break;
+    case 4: launch_segments<T, 4>(pl, a, st); break;
+    case 5: launch_segments<T, 5>(pl, a, st); break;
+    case 6: launch_segments<T, 6>(pl, a, st); break;
+    case 7: launch_segments<T, 7>(pl, a, st); break;
+    case 8: launch_segments<T, 8>(pl, a, st); break;
+    case 16: launch_segments<T, 16>(pl, a, st); break;
+    default: throw Unsupported("local_k has no specialised stage-1 kernel");
+  }
+}
+
+template <int KP>
+void launch_merge(const uint32_t* in, uint32_t parts, uint64_t rows, uint64_t B, float* gv, uint32_t* gi,
+                  uint64_t gstride, uint32_t* summ_out, const uint32_t* prefix, cudaStream_t st) {
+  const uint64_t threads = rows * B;
+  merge_finalize_kernel<KP><<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, st>>>(
+      in, parts, rows, B, gv, gi, gstride, summ_out, prefix);
+  check_launch();
+}
+
+void dispatch_merge(uint32_t kp, const uint32_t* in, uint32_t parts, uint64_t rows, uint64_t B, float* gv,
+                    uint32_t* gi, uint64_t gstride, uint32_t* summ_out, cudaStream_t st,
+                    const uint32_t* prefix = nullptr) {
+  switch (kp) {
+    case 1: launch_merge<1>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
+    case 2: launch_merge<2>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
+    case 3: launch_merge<3>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
+    case 4: launch_merge<4>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
+    case 5: launch_merge<5>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
+    case 6: launch_merge<6>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
+    case 7: launch_merge<7>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
+    case 8: launch_merge<8>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
+    case 16: launch_merge<16>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
+    default: throw Unsupported("local_k has no specialised merge kernel");
+  }
+}
+
+uint64_t stage1_ws_bytes(const S1Plan& pl, uint64_t rows, uint64_t B, uint32_t kp) {
+  if (pl.generic) return 0;
+  return align_up(rows * pl.cpr * (2ull * kp + 2) * B * 4);
+}
+
+// stage 1 into a grid (grid_stride elements between rows)
+void run_stage1_grid(int dtype, const void* in, uint64_t rows, const atkg_params& p, float* gv, uint32_t* gi,
+                     uint64_t gstride, void* ws, uint32_t* status, cudaStream_t st) {
+  const uint64_t B = p.num_buckets;
+  const uint32_t kp = p.local_k;
+  const S1Plan pl = plan_stage1(dtype, in, rows, p.n, p.n, B, kp);
+  if (pl.generic) {
+    if (gstride != kp * B) throw Unsupported("generic stage 1 needs a dense grid");
+    const uint64_t threads = rows * B;
+    if (dtype == ATKG_BF16)
+      stage1_generic_kernel<__nv_bfloat16><<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(in), rows, p.n, B, kp, gv, gi, status);
+    else
+      stage1_generic_kernel<float><<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, st>>>(
+          static_cast<const float*>(in), rows, p.n, B, kp, gv, gi, status);
+    check_launch();
+    return;
+  }
+  SegArgs a{};
+  a.in = in;
+  a.row_stride = p.n;
+  a.rows = rows;
+  a.B = B;
+  a.nstr = pl.nstr;
+  a.index_offset = 0;
+  a.seg_len = pl.seg_len;
+  a.segs = pl.segs;
+  a.cta_per_row_tile = pl.cpr;
+  a.tiles = pl.tiles;
+  a.out = static_cast<uint32_t*>(ws);
+  a.status = status;
+  if (dtype == ATKG_BF16) dispatch_segments<__nv_bfloat16>(kp, pl, a, st);
+  else dispatch_segments<float>(kp, pl, a, st);
+  dispatch_merge(kp, a.out, pl.cpr, rows, B, gv, gi, gstride, nullptr, st);
+}
+
+// ---------------------------------------------------------------------------
+// stage 2 / exact selection
+// ---------------------------------------------------------------------------
+uint64_t radix_ws_bytes(uint64_t rows, uint32_t k) {
+  return align_up(rows * sizeof(RowSel)) + align_up(rows * 256 * 4) + align_up(rows * (uint64_t)k * 8);
+}
+
+template <class Src>
+void run_radix(const Src& src, uint64_t rows, uint64_t count, uint32_t k, float* ov, uint32_t* oi, void* ws,
+               uint32_t* status, cudaStream_t st) {
+  if (k > kMaxSortKeys) throw Unsupported("k above 16384 is not supported by the device selection path");
+  char* w = static_cast<char*>(ws);
+  RowSel* sel = reinterpret_cast<RowSel*>(w);
+  w += align_up(rows * sizeof(RowSel));
+  uint32_t* hist = reinterpret_cast<uint32_t*>(w);
+  w += align_up(rows * 256 * 4);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(w);
+  radix_init_kernel<<<static_cast<unsigned>(std::max<uint64_t>(1, ceil_div(rows * 256, 256))), 256, 0, st>>>(
+      sel, hist, rows, k);
+  check_launch();
+  const uint64_t ctas_total = static_cast<uint64_t>(sm_count()) * 8;
+  uint64_t cpr = std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(count, 4096), ceil_div(ctas_total, rows)));
+  const dim3 grid(static_cast<unsigned>(cpr), static_cast<unsigned>(rows));
+  for (int pass = 0; pass < 8; ++pass) {
+    radix_hist_kernel<Src><<<grid, 256, 0, st>>>(src, pass, sel, hist, status);
+    check_launch();
+    radix_select_kernel<<<static_cast<unsigned>(ceil_div(rows, 8)), 256, 0, st>>>(pass, sel, hist, rows, status);
+    check_launch();
+  }
+  radix_gather_kernel<Src><<<grid, 256, 0, st>>>(src, sel, keys, k);
+  check_launch();
+  const uint32_t P = next_pow2(k);
+  static bool attr = false;
+  if (!attr) {
+    CUDA_OK(cudaFuncSetAttribute(sort_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSortKeys * 8));
+    attr = true;
+  }
+  sort_emit_kernel<<<static_cast<unsigned>(rows), std::min<uint32_t>(1024, P / 2), P * 8, st>>>(keys, k, P, ov, oi,
+                                                                                             status);
+  check_launch();
+}
+
+uint64_t select_ws_bytes(uint64_t rows, uint64_t count, uint32_t k) {
+  if (next_pow2(count) <= kMaxSortKeys) return 0;
+  return radix_ws_bytes(rows, k);
+}
+
+void run_select(const float* vals, const uint32_t* idx, uint64_t rows, uint64_t count, uint64_t stride, uint32_t k,
+                uint64_t limit, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st) {
+  const uint32_t P = next_pow2(count);
+  if (P <= kMaxSortKeys) {
+    static bool attr = false;
+    if (!attr) {
+      CUDA_OK(cudaFuncSetAttribute(stage2_bitonic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kMaxSortKeys * 8));
+      attr = true;
+    }
+    stage2_bitonic_kernel<<<static_cast<unsigned>(rows), std::min<uint32_t>(1024, P / 2), P * 8, st>>>(
+        vals, idx, count, stride, k, limit, P, ov, oi, status);
+    check_launch();
+    return;
+  }
+  CandSrc src{vals, idx, count, stride, limit};
+  run_radix(src, rows, count, k, ov, oi, ws, status, st);
+}
+
+uint64_t grid_bytes(uint64_t rows, const atkg_params& p) { return align_up(rows * p.local_k * p.num_buckets * 8); }
+
+uint64_t filled_count(const atkg_params& p) {  // topk.cpp:250-253
+  return std::min<uint64_t>(p.local_k, p.n / p.num_buckets) * p.num_buckets;
+}
+
+// ---------------------------------------------------------------------------
+// device scratch cache for the host-buffer entry points
+// ---------------------------------------------------------------------------
+struct HostCtx {
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  void* buf[6] = {};
+  size_t cap[6] = {};
+  void* get(int slot, size_t bytes) {
+    if (bytes == 0) bytes = 256;
+    if (cap[slot] < bytes) {
+      if (buf[slot]) CUDA_OK(cudaFree(buf[slot]));
+      CUDA_OK(cudaMalloc(&buf[slot], bytes));
+      cap[slot] = bytes;
+    }
+    return buf[slot];
+  }
+  cudaStream_t s() {
+    if (!stream) CUDA_OK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    return stream;
+  }
+};
+HostCtx& host_ctx() {
+  static HostCtx* c = new HostCtx();
+  return *c;
+}
+
+void check_status_sync(const uint32_t* d_status, cudaStream_t st) {
+  uint32_t flags = 0;
+  CUDA_OK(cudaMemcpyAsync(&flags, d_status, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaStreamSynchronize(st));
+  if (flags & ATKG_FLAG_NAN) throw NanInput();
+  if (flags & kFlagFew) throw_inval("fewer candidates than k");
+}
+
+}  // namespace atkg
+
+using namespace atkg;
+
+// ===========================================================================
+extern "C" {
+
+const char* atkg_last_error(void) { return g_last_error.c_str(); }
+const char* atkg_version(void) { return "atkg 0.1 (sm_100a)"; }
+
+int atkg_validate(const atkg_params* p) {
+  return guarded([&] { validate(*p); });
+}
+
+int atkg_workspace_size(int op, int dtype, uint64_t rows, const atkg_params* p, size_t* bytes) {
+  return guarded([&] {
+    const void* aligned = reinterpret_cast<const void*>(static_cast<uintptr_t>(256));
+    switch (op) {
+      case ATKG_OP_STAGE1: {
+        const S1Plan pl = plan_stage1(dtype, aligned, rows, p->n, p->n, p->num_buckets, p->local_k);
+        *bytes = stage1_ws_bytes(pl, rows, p->num_buckets, p->local_k);
+        break;
+      }
+      case ATKG_OP_APPROX: {
+        const S1Plan pl = plan_stage1(dtype, aligned, rows, p->n, p->n, p->num_buckets, p->local_k);
+        *bytes = stage1_ws_bytes(pl, rows, p->num_buckets, p->local_k) + grid_bytes(rows, *p) +
+                 select_ws_bytes(rows, filled_count(*p), p->global_k);
+        break;
+      }
+      case ATKG_OP_SELECT:
+        *bytes = select_ws_bytes(rows, p->n, p->global_k);
+        break;
+      case ATKG_OP_EXACT:
+        *bytes = radix_ws_bytes(rows, p->global_k);
+        break;
+      case ATKG_OP_SUMMARY: {
+        const S1Plan pl = plan_stage1(dtype, aligned, 1, p->n, p->n, p->num_buckets, p->local_k);
+        *bytes = stage1_ws_bytes(pl, 1, p->num_buckets, p->local_k);
+        break;
+      }
+      case ATKG_OP_MERGE:
+        *bytes = grid_bytes(1, *p) + select_ws_bytes(1, filled_count(*p), p->global_k);
+        break;
+      default:
+        throw_inval("unknown workspace op");
+    }
+    // slack so every device path can align its pointers
+    *bytes += 512;
+  });
+}
+
+int atkg_stage1(int dtype, const void* d_in, uint64_t rows, const atkg_params* p, float* d_grid_vals,
+                uint32_t* d_grid_idx, void* d_ws, size_t ws_bytes, uint32_t* d_status, void* stream) {
+  return guarded([&] {
+    validate(*p);
+    if (rows == 0) return;
+    (void)ws_bytes;
+    run_stage1_grid(dtype, d_in, rows, *p, d_grid_vals, d_grid_idx, (uint64_t)p->local_k * p->num_buckets, d_ws,
+                    d_status, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int atkg_select_candidates(const float* d_vals, const uint32_t* d_idx, uint64_t rows, uint64_t count,
+                           uint64_t stride, uint32_t k, uint64_t index_limit, float* d_out_vals,
+                           uint32_t* d_out_idx, void* d_ws, size_t ws_bytes, uint32_t* d_status, void* stream) {
+  return guarded([&] {
+    if (k == 0) throw_inval("k must be >= 1");
+    if (rows == 0) return;
+    if (count < k) throw_inval("fewer candidates than k");
+    (void)ws_bytes;
+    run_select(d_vals, d_idx, rows, count, stride, k, index_limit, d_out_vals, d_out_idx, d_ws, d_status,
+               static_cast<cudaStream_t>(stream));
+  });
+}
+
+int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_params* p, float* d_out_vals,
+                      uint32_t* d_out_idx, void* d_ws, size_t ws_bytes, uint32_t* d_status, void* stream) {
+  return guarded([&] {
+    validate(*p);
+    if (rows == 0) return;
+    (void)ws_bytes;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const S1Plan pl = plan_stage1(dtype, d_in, rows, p->n, p->n, p->num_buckets, p->local_k);
+    char* w = static_cast<char*>(d_ws);
+    w = reinterpret_cast<char*>(align_up(reinterpret_cast<uintptr_t>(w)));
+    void* s1ws = w;
+    w += stage1_ws_bytes(pl, rows, p->num_buckets, p->local_k);
+    const uint64_t gstride = (uint64_t)p->local_k * p->num_buckets;
+    float* gv = reinterpret_cast<float*>(w);
+    uint32_t* gi = reinterpret_cast<uint32_t*>(w + rows * gstride * 4);
+    w += grid_bytes(rows, *p);
+    run_stage1_grid(dtype, d_in, rows, *p, gv, gi, gstride, s1ws, d_status, st);
+    run_select(gv, gi, rows, filled_count(*p), gstride, p->global_k, UINT64_MAX, d_out_vals, d_out_idx, w,
+               d_status, st);
+  });
+}
+
+int atkg_exact_top_k(int dtype, const void* d_in, uint64_t rows, uint64_t n, uint32_t k, float* d_out_vals,
+                     uint32_t* d_out_idx, void* d_ws, size_t ws_bytes, uint32_t* d_status, void* stream) {
+  return guarded([&] {
+    if (k == 0) throw_inval("k must be >= 1");
+    if (n > 0xffffffffull + 1) throw_inval("input exceeds the 32-bit index range");
+    if (k > n) throw_inval("k must not exceed the input length");
+    if (rows == 0) return;
+    (void)ws_bytes;
+    char* w = reinterpret_cast<char*>(align_up(reinterpret_cast<uintptr_t>(d_ws)));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dtype == ATKG_BF16) {
+      DenseSrc<__nv_bfloat16> src{static_cast<const __nv_bfloat16*>(d_in), n};
+      run_radix(src, rows, n, k, d_out_vals, d_out_idx, w, d_status, st);
+    } else {
+      DenseSrc<float> src{static_cast<const float*>(d_in), n};
+      run_radix(src, rows, n, k, d_out_vals, d_out_idx, w, d_status, st);
+    }
+  });
+}
+
+int atkg_stage1_summary(int dtype, const void* d_slice, uint64_t len, uint64_t index_offset, const atkg_params* p,
+                        uint32_t* d_summary, void* d_ws, size_t ws_bytes, uint32_t* d_status, void* stream) {
+  return guarded([&] {
+    validate(*p);
+    const uint64_t B = p->num_buckets;
+    if (len % B != 0 || index_offset % B != 0) throw_inval("slice length and offset must be multiples of num_buckets");
+    if (index_offset + len > p->n) throw_inval("slice exceeds the row");
+    (void)ws_bytes;
+    if (!kp_specialised(p->local_k)) throw Unsupported("local_k has no specialised summary kernel");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const S1Plan pl = plan_stage1(dtype, d_slice, 1, len, len, B, p->local_k);
+    if (pl.generic) throw Unsupported("summary path needs num_buckets % 4 == 0 and aligned input");
+    char* w = reinterpret_cast<char*>(align_up(reinterpret_cast<uintptr_t>(d_ws)));
+    SegArgs a{};
+    a.in = d_slice;
+    a.row_stride = len;
+    a.rows = 1;
+    a.B = B;
+    a.nstr = pl.nstr;
+    a.index_offset = index_offset;
+    a.seg_len = pl.seg_len;
+    a.segs = pl.segs;
+    a.cta_per_row_tile = pl.cpr;
+    a.tiles = pl.tiles;
+    a.out = reinterpret_cast<uint32_t*>(w);
+    a.status = d_status;
+    if (dtype == ATKG_BF16) dispatch_segments<__nv_bfloat16>(p->local_k, pl, a, st);
+    else dispatch_segments<float>(p->local_k, pl, a, st);
+    dispatch_merge(p->local_k, a.out, pl.cpr, 1, B, nullptr, nullptr, 0, d_summary, st);
+  });
+}
+
+int atkg_summary_merge_top_k(const uint32_t* d_summaries, uint32_t parts, const atkg_params* p, float* d_grid_vals,
+                             uint32_t* d_grid_idx, float* d_out_vals, uint32_t* d_out_idx, void* d_ws,
+                             size_t ws_bytes, uint32_t* d_status, void* stream) {
+  return guarded([&] {
+    validate(*p);
+    if (parts == 0) throw_inval("need at least one summary");
+    if (!kp_specialised(p->local_k)) throw Unsupported("local_k has no specialised merge kernel");
+    (void)ws_bytes;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    char* w = reinterpret_cast<char*>(align_up(reinterpret_cast<uintptr_t>(d_ws)));
+    const uint64_t gstride = (uint64_t)p->local_k * p->num_buckets;
+    float* gv = d_grid_vals;
+    uint32_t* gi = d_grid_idx;
+    if (!gv) {
+      gv = reinterpret_cast<float*>(w);
+      gi = reinterpret_cast<uint32_t*>(w + gstride * 4);
+    }
+    w += grid_bytes(1, *p);
+    dispatch_merge(p->local_k, d_summaries, parts, 1, p->num_buckets, gv, gi, gstride, nullptr, st);
+    if (d_out_vals)
+      run_select(gv, gi, 1, filled_count(*p), gstride, p->global_k, UINT64_MAX, d_out_vals, d_out_idx, w, d_status,
+                 st);
+  });
+}
+
+int atkg_check_status(const uint32_t* d_status, void* stream) {
+  return guarded([&] { check_status_sync(d_status, static_cast<cudaStream_t>(stream)); });
+}
+
+// ---- host-buffer drop-in ----------------------------------------------------
+int atkg_stage1_host(const float* in, uint64_t rows, const atkg_params* p, float* grid_vals, uint32_t* grid_idx) {
+  return guarded([&] {
+    validate(*p);
+    HostCtx& c = host_ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    cudaStream_t st = c.s();
+    size_t ws = 0;
+    if (int rc = atkg_workspace_size(ATKG_OP_STAGE1, ATKG_F32, rows, p, &ws)) throw Inval(g_last_error);
+    const uint64_t nin = rows * p->n, ng = rows * p->local_k * p->num_buckets;
+    float* din = static_cast<float*>(c.get(0, nin * 4));
+    float* gv = static_cast<float*>(c.get(1, ng * 4));
+    uint32_t* gi = static_cast<uint32_t*>(c.get(2, ng * 4));
+    void* dws = c.get(3, ws);
+    uint32_t* status = static_cast<uint32_t*>(c.get(4, 4));
+    CUDA_OK(cudaMemsetAsync(status, 0, 4, st));
+    CUDA_OK(cudaMemcpyAsync(din, in, nin * 4, cudaMemcpyHostToDevice, st));
+    run_stage1_grid(ATKG_F32, din, rows, *p, gv, gi, p->local_k * p->num_buckets, dws, status, st);
+    check_status_sync(status, st);
+    CUDA_OK(cudaMemcpyAsync(grid_vals, gv, ng * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(grid_idx, gi, ng * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+  });
+}
+
+int atkg_select_candidates_host(const float* vals, const uint32_t* idx, uint64_t count, uint32_t k,
+                                uint64_t index_limit, float* out_vals, uint32_t* out_idx) {
+  return guarded([&] {
+    if (k == 0) throw_inval("k must be >= 1");
+    if (count < k) {
+      // NaN is rejected before the count check (topk.cpp:225-234)
+      for (uint64_t i = 0; i < count; ++i)
+        if (vals[i] != vals[i]) throw NanInput();
+      throw_inval("fewer candidates than k");
+    }
+    HostCtx& c = host_ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    cudaStream_t st = c.s();
+    float* dv = static_cast<float*>(c.get(0, count * 4));
+    uint32_t* di = static_cast<uint32_t*>(c.get(1, count * 4));
+    float* ov = static_cast<float*>(c.get(2, (uint64_t)k * 4));
+    uint32_t* oi = static_cast<uint32_t*>(c.get(3, (uint64_t)k * 4));
+    void* dws = c.get(5, select_ws_bytes(1, count, k) + 512);
+    uint32_t* status = static_cast<uint32_t*>(c.get(4, 4));
+    CUDA_OK(cudaMemsetAsync(status, 0, 4, st));
+    CUDA_OK(cudaMemcpyAsync(dv, vals, count * 4, cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(di, idx, count * 4, cudaMemcpyHostToDevice, st));
+    run_select(dv, di, 1, count, count, k, index_limit, ov, oi,
+               reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(dws))), status, st);
+    check_status_sync(status, st);
+    CUDA_OK(cudaMemcpyAsync(out_vals, ov, (uint64_t)k * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(out_idx, oi, (uint64_t)k * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+  });
+}
+
+int atkg_approx_top_k_host(const float* rows_in, uint64_t rows, const atkg_params* p, float* out_vals,
+                           uint32_t* out_idx) {
+  return guarded([&] {
+    validate(*p);
+    if (rows == 0) return;
+    HostCtx& c = host_ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    cudaStream_t st = c.s();
+    size_t ws = 0;
+    if (atkg_workspace_size(ATKG_OP_APPROX, ATKG_F32, rows, p, &ws)) throw Inval(g_last_error);
+    const uint64_t nin = rows * p->n, no = rows * p->global_k;
+    float* din = static_cast<float*>(c.get(0, nin * 4));
+    float* ov = static_cast<float*>(c.get(1, no * 4));
+    uint32_t* oi = static_cast<uint32_t*>(c.get(2, no * 4));
+    void* dws = c.get(3, ws);
+    uint32_t* status = static_cast<uint32_t*>(c.get(4, 4));
+    CUDA_OK(cudaMemsetAsync(status, 0, 4, st));
+    CUDA_OK(cudaMemcpyAsync(din, rows_in, nin * 4, cudaMemcpyHostToDevice, st));
+    const int rc = atkg_approx_top_k(ATKG_F32, din, rows, p, ov, oi, dws, ws, status, st);
+    if (rc) throw Inval(g_last_error);
+    check_status_sync(status, st);
+    CUDA_OK(cudaMemcpyAsync(out_vals, ov, no * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(out_idx, oi, no * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+  });
+}
+
+int atkg_exact_top_k_host(const float* in, uint64_t n, uint32_t k, float* out_vals, uint32_t* out_idx) {
+  return guarded([&] {
+    if (k == 0) throw_inval("k must be >= 1");
+    if (n > 0xffffffffull + 1) throw_inval("input exceeds the 32-bit index range");
+    if (k > n) throw_inval("k must not exceed the input length");
+    HostCtx& c = host_ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    cudaStream_t st = c.s();
+    float* din = static_cast<float*>(c.get(0, n * 4));
+    float* ov = static_cast<float*>(c.get(1, (uint64_t)k * 4));
+    uint32_t* oi = static_cast<uint32_t*>(c.get(2, (uint64_t)k * 4));
+    void* dws = c.get(3, radix_ws_bytes(1, k) + 512);
+    uint32_t* status = static_cast<uint32_t*>(c.get(4, 4));
+    CUDA_OK(cudaMemsetAsync(status, 0, 4, st));
+    CUDA_OK(cudaMemcpyAsync(din, in, n * 4, cudaMemcpyHostToDevice, st));
+    DenseSrc<float> src{din, n};
+    run_radix(src, 1, n, k, ov, oi, reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(dws))), status, st);
+    check_status_sync(status, st);
+    CUDA_OK(cudaMemcpyAsync(out_vals, ov, (uint64_t)k * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(out_idx, oi, (uint64_t)k * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+  });
+}
+
+// measure_recall (topk.cpp:275-297): |approx ∩ exact| / K by sorted merge
+int atkg_measure_recall(const uint32_t* approx_idx, uint64_t approx_k, const uint32_t* exact_idx,
+                        uint64_t exact_k, double* out) {
+  return guarded([&] {
+    if (approx_k != exact_k) throw_inval("recall needs results of equal size");
+    if (approx_k == 0) throw_inval("recall of empty results is undefined");
+    std::vector<uint32_t> a(approx_idx, approx_idx + approx_k), b(exact_idx, exact_idx + exact_k);
+    std::sort(a.begin(), a.end());
+    std::sort(b.begin(), b.end());
+    uint64_t hits = 0, i = 0, j = 0;
+    while (i < a.size() && j < b.size()) {
+      if (a[i] < b[j]) ++i;
+      else if (b[j] < a[i]) ++j;
+      else { ++hits; ++i; ++j; }
+    }
+    *out = static_cast<double>(hits) / static_cast<double>(exact_k);
+  });
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// streaming accumulator (Stage1Accumulator, include/atk/topk.hpp:68-94)
+// ===========================================================================
+struct atkg_accumulator {
+  atkg_params p;
+  uint64_t consumed = 0;
+  bool summary_mode = false;
+  uint32_t* summ = nullptr;   // summary mode: (2kp+2)*B words
+  float* gv = nullptr;        // grid mode / candidates scratch
+  uint32_t* gi = nullptr;
+  uint32_t* status = nullptr;
+  void* ws = nullptr;         // segment-kernel scratch for aligned bodies
+  size_t ws_cap = 0;
+};
+
+namespace atkg {
+
+template <int KP>
+void launch_clear(uint32_t* summ, uint64_t B, cudaStream_t st) {
+  summary_clear_kernel<KP><<<static_cast<unsigned>(ceil_div(B, 128)), 128, 0, st>>>(summ, B);
+  check_launch();
+}
+template <typename T, int KP>
+void launch_fold(uint32_t* summ, uint64_t B, const void* blk, uint64_t start, uint64_t count, uint32_t* status,
+                 cudaStream_t st) {
+  fold_summary_kernel<T, KP><<<static_cast<unsigned>(ceil_div(B, 128)), 128, 0, st>>>(
+      summ, B, static_cast<const T*>(blk), start, count, status);
+  check_launch();
+}
+#define ATKG_KP_SWITCH(kp, CALL)                   \
+  switch (kp) {                                    \
+    case 1: { constexpr int K_ = 1; CALL; } break;  \
+    case 2: { constexpr int K_ = 2; CALL; } break;  \
+    case 3: { constexpr int K_ = 3; CALL; } break;  \
+    case 4: { constexpr int K_ = 4; CALL; } break;  \
+    case 5: { constexpr int K_ = 5; CALL; } break;  \
+    case 6: { constexpr int K_ = 6; CALL; } break;  \
+    case 7: { constexpr int K_ = 7; CALL; } break;  \
+    case 8: { constexpr int K_ = 8; CALL; } break;  \
+    case 16: { constexpr int K_ = 16; CALL; } break; \
+    default: throw Unsupported("local_k has no specialised kernel"); \
+  }
+
+void acc_fold(atkg_accumulator* a, int dtype, const void* blk, uint64_t start, uint64_t count, cudaStream_t st) {
+  if (count == 0) return;
+  const uint64_t B = a->p.num_buckets;
+  if (a->summary_mode) {
+    if (dtype == ATKG_BF16) { ATKG_KP_SWITCH(a->p.local_k, (launch_fold<__nv_bfloat16, K_>(a->summ, B, blk, start, count, a->status, st))); }
+    else { ATKG_KP_SWITCH(a->p.local_k, (launch_fold<float, K_>(a->summ, B, blk, start, count, a->status, st))); }
+  } else {
+    if (dtype == ATKG_BF16)
+      fold_grid_kernel<__nv_bfloat16><<<static_cast<unsigned>(ceil_div(B, 128)), 128, 0, st>>>(
+          a->gv, a->gi, B, a->p.local_k, static_cast<const __nv_bfloat16*>(blk), start, count, a->status);
+    else
+      fold_grid_kernel<float><<<static_cast<unsigned>(ceil_div(B, 128)), 128, 0, st>>>(
+          a->gv, a->gi, B, a->p.local_k, static_cast<const float*>(blk), start, count, a->status);
+    check_launch();
+  }
+}
+
+}  // namespace atkg
+
+extern "C" {
+
+int atkg_accumulator_create(const atkg_params* p, atkg_accumulator** out) {
+  return guarded([&] {
+    validate(*p);
+    auto* a = new atkg_accumulator();
+    a->p = *p;
+    const uint64_t B = p->num_buckets, kp = p->local_k;
+    a->summary_mode = kp_specialised(p->local_k);
+    CUDA_OK(cudaMalloc(&a->status, 4));
+    CUDA_OK(cudaMemset(a->status, 0, 4));
+    CUDA_OK(cudaMalloc(&a->gv, kp * B * 4));
+    CUDA_OK(cudaMalloc(&a->gi, kp * B * 4));
+    if (a->summary_mode) {
+      CUDA_OK(cudaMalloc(&a->summ, (2 * kp + 2) * B * 4));
+      ATKG_KP_SWITCH(p->local_k, (launch_clear<K_>(a->summ, B, 0)));
+    } else {
+      grid_init_kernel<<<static_cast<unsigned>(ceil_div(kp * B, 256)), 256>>>(a->gv, a->gi, kp * B);
+      check_launch();
+    }
+    CUDA_OK(cudaDeviceSynchronize());
+    *out = a;
+  });
+}
+
+// consume(): positions consumed()..+len-1, any length and alignment
+// (topk.cpp:123-172).  The bucket-aligned body of a large block runs through
+// the segment kernels; ragged edges and odd layouts fold element-wise.
+int atkg_accumulator_consume(atkg_accumulator* a, int dtype, const void* d_block, uint64_t len, void* stream) {
+  return guarded([&] {
+    if (a->consumed + len > a->p.n) throw_inval("stage 1 fed more than n elements");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t B = a->p.num_buckets;
+    const uint64_t esz = dtype == ATKG_BF16 ? 2 : 4;
+    const char* blk = static_cast<const char*>(d_block);
+    uint64_t start = a->consumed;
+    const uint64_t end = start + len;
+    if (a->summary_mode && len >= 4 * B) {
+      const uint64_t h = std::min(end, ceil_div(start, B) * B);
+      acc_fold(a, dtype, blk, start, h - start, st);
+      const uint64_t body = (end - h) / B * B;
+      const void* bptr = blk + (h - start) * esz;
+      const S1Plan pl = plan_stage1(dtype, bptr, 1, body, body, B, a->p.local_k);
+      if (body > 0 && !pl.generic) {
+        const size_t need = stage1_ws_bytes(pl, 1, B, a->p.local_k);
+        if (a->ws_cap < need) {
+          if (a->ws) CUDA_OK(cudaFree(a->ws));
+          CUDA_OK(cudaMalloc(&a->ws, need));
+          a->ws_cap = need;
+        }
+        SegArgs s{};
+        s.in = bptr;
+        s.row_stride = body;
+        s.rows = 1;
+        s.B = B;
+        s.nstr = pl.nstr;
+        s.index_offset = h;
+        s.seg_len = pl.seg_len;
+        s.segs = pl.segs;
+        s.cta_per_row_tile = pl.cpr;
+        s.tiles = pl.tiles;
+        s.out = static_cast<uint32_t*>(a->ws);
+        s.status = a->status;
+        if (dtype == ATKG_BF16) dispatch_segments<__nv_bfloat16>(a->p.local_k, pl, s, st);
+        else dispatch_segments<float>(a->p.local_k, pl, s, st);
+        dispatch_merge(a->p.local_k, s.out, pl.cpr, 1, B, nullptr, nullptr, 0, a->summ, st, a->summ);
+        acc_fold(a, dtype, blk + (h + body - start) * esz, h + body, end - h - body, st);
+      } else {
+        acc_fold(a, dtype, blk + (h - start) * esz, h, end - h, st);
+      }
+    } else {
+      acc_fold(a, dtype, blk, start, len, st);
+    }
+    a->consumed = end;
+  });
+}
+
+uint64_t atkg_accumulator_consumed(const atkg_accumulator* a) { return a->consumed; }
+
+int atkg_accumulator_candidates(atkg_accumulator* a, float* d_vals, uint32_t* d_idx, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t B = a->p.num_buckets, kp = a->p.local_k;
+    if (a->summary_mode) {
+      dispatch_merge(a->p.local_k, a->summ, 1, 1, B, d_vals, d_idx, kp * B, nullptr, st);
+    } else {
+      CUDA_OK(cudaMemcpyAsync(d_vals, a->gv, kp * B * 4, cudaMemcpyDeviceToDevice, st));
+      CUDA_OK(cudaMemcpyAsync(d_idx, a->gi, kp * B * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    check_status_sync(a->status, st);
+  });
+}
+
+void atkg_accumulator_destroy(atkg_accumulator* a) {
+  if (!a) return;
+  cudaFree(a->summ);
+  cudaFree(a->gv);
+  cudaFree(a->gi);
+  cudaFree(a->status);
+  cudaFree(a->ws);
+  delete a;
+}
+
+}  // extern "C"

@@ -1,0 +1,229 @@
+"""Pins the CPU oracle (oracle/atk_oracle.c) before it is trusted.
+
+(a) the reference's own known-answer tests, restated from
+    proj/tests/test_topk.cpp, test_planner.cpp, test_recall.cpp;
+(b) the committed golden fixtures, produced by the reference library itself
+    (tests/golden/make_golden.py over oracle/_ref);
+(c) direct comparison with oracle/_ref where it is built (this container and
+    the GPU box).
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+from tests.golden.inputs import INPUTS, build
+
+INF = np.float32(np.inf)
+
+
+def bits(a):
+    return np.asarray(a, np.float32).view(np.uint32)
+
+
+# ---- test_topk.cpp KATs -------------------------------------------------------
+def test_update_bucket_traces(port):
+    # test_topk.cpp:83-120
+    v = np.full(2, -INF, np.float32)
+    i = np.zeros(2, np.uint32)
+    for idx, x in enumerate([9, 7, 4]):
+        v, i = port.update_bucket(v, i, x, idx)
+    assert list(v) == [9, 7] and list(i) == [0, 1]
+    v, i = port.update_bucket(v, i, 8, 3)
+    assert list(v) == [9, 8] and list(i) == [0, 3]
+    v = np.full(2, -INF, np.float32); i = np.zeros(2, np.uint32)
+    for idx, x in enumerate([3, 1, 4, 1, 5]):
+        v, i = port.update_bucket(v, i, x, idx)
+    assert list(v) == [5, 4] and list(i) == [4, 2]
+    # ties: a later equal value replaces the minimum slot
+    v = np.full(2, -INF, np.float32); i = np.zeros(2, np.uint32)
+    for idx, x in enumerate([5, 3, 3]):
+        v, i = port.update_bucket(v, i, x, idx)
+    assert list(v) == [5, 3] and list(i) == [0, 2]
+    # ties: the bubble pass never passes an equal value
+    v = np.full(2, -INF, np.float32); i = np.zeros(2, np.uint32)
+    for idx, x in enumerate([3, 1, 3]):
+        v, i = port.update_bucket(v, i, x, idx)
+    assert list(v) == [3, 3] and list(i) == [0, 2]
+
+
+def test_stage1_worked_example(port):
+    # test_topk.cpp:138-143
+    v, i = port.stage1(np.array([3, 1, 4, 1, 5, 9, 2, 6], np.float32), 2, 1, lane=1)
+    assert list(v) == [5, 9] and list(i) == [4, 5]
+
+
+@pytest.mark.parametrize("n,b,kp", [(64, 8, 1), (64, 8, 3), (60, 5, 2), (1024, 128, 4), (96, 4, 7), (33, 3, 2),
+                                    (4096, 16, 5)])
+def test_stage1_layout_vs_bucket_sort(port, n, b, kp):
+    # test_topk.cpp:145-175 (distinct values, bucket-minor layout)
+    from oracle.pyoracle import shuffled_iota
+    row = shuffled_iota(n, 1000 + n + kp)
+    v, i = port.stage1(row, b, kp, lane=1)
+    s = n // b
+    for bk in range(b):
+        members = sorted(((row[j], j) for j in range(bk, n, b)), key=lambda t: -t[0])
+        for k in range(kp):
+            if k < s:
+                assert v[k * b + bk] == members[k][0] and i[k * b + bk] == members[k][1]
+            else:
+                assert v[k * b + bk] == -INF and i[k * b + bk] == 0
+
+
+def test_stage1_duplicate_heavy_vs_scalar(port):
+    # test_topk.cpp:190-210
+    from oracle.pyoracle import uniform_below
+    row = uniform_below(99, 17, 4096)
+    B, kp = 32, 3
+    gv, gi = port.stage1(row, B, kp, lane=1)
+    state = [(np.full(kp, -INF, np.float32), np.zeros(kp, np.uint32)) for _ in range(B)]
+    for idx, x in enumerate(row):
+        v, i = state[idx % B]
+        state[idx % B] = port.update_bucket(v, i, x, idx)
+    for bk in range(B):
+        for k in range(kp):
+            assert bits(gv[k * B + bk]) == bits(state[bk][0][k])
+            assert gi[k * B + bk] == state[bk][1][k]
+
+
+def test_approx_worked_example(port):
+    # test_topk.cpp:259-264
+    v, i = port.approx_top_k(np.array([5, 1, 7, 3, 9, 2, 8, 4], np.float32), 4, 2, 3, lane=1)
+    assert list(v) == [9, 8, 7] and list(i) == [4, 6, 2]
+
+
+def test_exact_tie_break_with_signed_zero_and_inf(port):
+    # test_topk.cpp:323-371
+    from oracle.pyoracle import uniform_below
+    v, i = port.exact_top_k(np.array([5, 3, 5], np.float32), 2)
+    assert list(v) == [5, 5] and list(i) == [0, 2]
+    base = uniform_below(4242, 41, 900) - np.float32(20)
+    row = np.concatenate([base, np.array([0.0, -0.0, np.inf, -np.inf], np.float32)]).astype(np.float32)
+    order = sorted(range(row.size), key=lambda a: (-float(row[a]), a))
+    v, i = port.exact_top_k(row, 101)
+    assert list(i) == order[:101]
+    assert all(v[t] == row[order[t]] for t in range(101))
+    v, i = port.exact_top_k(np.array([2, 8, 1], np.float32), 3)
+    assert list(v) == [8, 2, 1] and list(i) == [1, 0, 2]
+    with pytest.raises(ValueError):
+        port.exact_top_k(np.array([1, 2, 3], np.float32), 0)
+    with pytest.raises(ValueError):
+        port.exact_top_k(np.array([1, 2, 3], np.float32), 4)
+    with pytest.raises(ValueError, match="NaN"):
+        port.exact_top_k(np.array([1, np.nan], np.float32), 1)
+
+
+def test_negative_zero_emitted_as_positive(port):
+    v, i = port.exact_top_k(np.array([-0.0, -1.0], np.float32), 1)
+    assert bits(v[0]) == 0 and i[0] == 0
+
+
+def test_select_index_limit(port):
+    # test_topk.cpp:373-381
+    v, i = port.select_candidates(np.array([9, 8, 7, 6], np.float32), np.array([10, 3, 11, 4], np.uint32), 2, 10)
+    assert list(v) == [8, 6] and list(i) == [3, 4]
+    with pytest.raises(ValueError, match="fewer candidates than k"):
+        port.select_candidates(np.array([9, 8, 7, 6], np.float32), np.array([10, 3, 11, 4], np.uint32), 3, 10)
+
+
+def test_measure_recall(port):
+    # test_topk.cpp:383-397
+    assert port.measure_recall([4, 2], [4, 2]) == 1.0
+    assert port.measure_recall([2, 4], [4, 2]) == 1.0
+    assert port.measure_recall([4, 7], [4, 2]) == 0.5
+    assert port.measure_recall([9, 8], [4, 2]) == 0.0
+    with pytest.raises(ValueError):
+        port.measure_recall([4], [4, 2])
+
+
+def test_validate_messages(port):
+    # test_topk.cpp:419-459, messages topk.cpp:54-67
+    port.validate(256, 16, 2, 20, 8)
+    for args, msg in [((0, 16, 2, 20, 8), "n must be >= 1"),
+                      ((1 << 32, 1 << 32, 2, 20, 8), "n exceeds the 32-bit index range"),
+                      ((256, 0, 2, 20, 8), "num_buckets must be >= 1"),
+                      ((256, 24, 2, 20, 8), "num_buckets must divide n"),
+                      ((256, 16, 2, 20, 3), "num_buckets must be a multiple of lane_multiple"),
+                      ((256, 16, 0, 20, 8), "local_k must be >= 1"),
+                      ((256, 16, 2, 0, 8), "global_k must be >= 1"),
+                      ((256, 16, 2, 257, 8), "global_k must not exceed n"),
+                      ((256, 16, 2, 40, 8), "num_buckets \\* local_k must be >= global_k")]:
+        with pytest.raises(ValueError, match=msg):
+            port.validate(*args)
+
+
+# ---- recall / planner KATs ----------------------------------------------------
+def test_planner_kats(port):
+    # test_planner.cpp:86-115
+    p = port.select_parameters(262144, 1024, 0.95, (1, 2, 3, 4), 128, 1)
+    assert (p.local_k, p.num_buckets) == (4, 512) and p.exact
+    assert abs(p.recall - 0.96295662533487147) < 1e-10
+    p = port.select_parameters(262144, 1024, 0.95, (1,), 128, 1)
+    assert (p.local_k, p.num_buckets) == (1, 16384)
+    assert abs(p.recall - 0.97125744566081484) < 1e-10
+    p = port.select_parameters(262144, 1024, 0.99, (1, 2, 3, 4), 128, 1)
+    assert (p.local_k, p.num_buckets) == (4, 1024)
+
+
+def test_legal_bucket_counts(port):
+    # test_planner.cpp:59-84
+    big = port.legal_bucket_counts(430080, 128)
+    assert len(big) == 48 and big[:5] == [430080, 215040, 143360, 107520, 86016] and big[-1] == 128
+    assert port.legal_bucket_counts(100, 128) == []
+    assert port.legal_bucket_counts(12, 1) == [12, 6, 4, 3, 2, 1]
+
+
+def test_exact_recall_frozen(port):
+    # test_recall.cpp:193-211
+    for n, b, kp, k, val in [(262144, 16384, 1, 1024, 0.97125744566081484), (262144, 512, 4, 1024, 0.96295662533487147),
+                             (430080, 5120, 2, 3360, 0.94910419031798787), (15360, 640, 4, 480, 0.99888007349153884)]:
+        assert abs(port.exact_expected_recall(n, b, kp, k) - val) < 1e-10
+
+
+# ---- golden fixtures (reference library outputs) --------------------------------
+@pytest.mark.parametrize("name", [k for k in INPUTS if INPUTS[k]["n"] * INPUTS[k]["rows"] <= 1 << 21])
+def test_port_matches_golden(port, stage_fixtures, name):
+    spec = INPUTS[name]
+    rows = build(spec)
+    assert hashlib.sha256(rows.tobytes()).hexdigest() == str(stage_fixtures[f"{name}/input_sha"]), \
+        "input generator drifted from the golden fixtures"
+    B, kp, k, lane = spec["B"], spec["kp"], spec["k"], spec.get("lane", 128)
+    for r in range(rows.shape[0]):
+        gv, gi = port.stage1(rows[r], B, kp, lane)
+        assert np.array_equal(bits(gv), bits(stage_fixtures[f"{name}/grid_v"][r]))
+        assert np.array_equal(gi, stage_fixtures[f"{name}/grid_i"][r])
+    av, ai = port.approx_top_k_batch(rows, B, kp, k, lane)
+    assert np.array_equal(bits(av), bits(stage_fixtures[f"{name}/approx_v"]))
+    assert np.array_equal(ai, stage_fixtures[f"{name}/approx_i"])
+    ev, ei = port.exact_top_k(rows[0], k)
+    assert np.array_equal(ei, stage_fixtures[f"{name}/exact_i"][0])
+
+
+def test_planner_golden(port, planner_fixtures):
+    for (n, k, t, seed, kps, kp, b, rec, ex) in planner_fixtures["plans"]:
+        if n > 1 << 24:
+            continue  # the giant row's MC sweep is slow in the C port; pinned by test_planner.py
+        p = port.select_parameters(int(n), int(k), float(t), tuple(int(x) for x in kps.split(",")), 128, int(seed))
+        assert (p.local_k, p.num_buckets) == (kp, b)
+        assert p.recall == rec
+    for (n, b, kp, k, val) in planner_fixtures["exact"]:
+        assert port.exact_expected_recall(int(n), int(b), int(kp), int(k)) == val
+    for (n, b, kp, k, trials, seed, m, s) in planner_fixtures["mc"]:
+        mm, ss = port.mc_expected_recall(int(n), int(b), int(kp), int(k), int(trials), int(seed))
+        assert mm == m and ss == s
+
+
+# ---- direct comparison with the compiled reference ------------------------------
+def test_port_matches_ref_random(port, ref):
+    rng = np.random.default_rng(5)
+    for t in range(300):
+        B = int(rng.integers(1, 9)); s = int(rng.integers(1, 40)); kp = int(rng.integers(1, 10))
+        n = B * s
+        row = rng.integers(0, 5, n).astype(np.float32) if t % 2 else rng.standard_normal(n).astype(np.float32)
+        a = port.stage1(row, B, kp, lane=1)
+        b = ref.stage1(row, B, kp, lane=1)
+        assert np.array_equal(bits(a[0]), bits(b[0])) and np.array_equal(a[1], b[1])
+        k = int(rng.integers(1, min(n, B * kp) + 1))
+        a = port.approx_top_k(row, B, kp, k, lane=1)
+        b = ref.approx_top_k(row, B, kp, k, lane=1)
+        assert np.array_equal(bits(a[0]), bits(b[0])) and np.array_equal(a[1], b[1])
