@@ -83,6 +83,9 @@ typedef struct atkg_params {
 
 const char* atkg_last_error(void);
 const char* atkg_version(void);
+/* Selects the CUDA device for subsequent calls on this host thread
+ * (cudaSetDevice of the library's runtime). */
+int atkg_set_device(int device);
 
 int atkg_validate(const atkg_params* p);
 int atkg_validate_analysis(const atkg_params* p);
@@ -227,6 +230,15 @@ void atkg_fill_normal(uint64_t seed, uint64_t count, float mean, float stddev, f
 /* round-to-nearest-even fp32 -> bf16 bits */
 void atkg_f32_to_bf16(const float* in, uint64_t count, uint16_t* out, uint32_t threads);
 void atkg_bf16_to_f32(const uint16_t* in, uint64_t count, float* out, uint32_t threads);
+
+/* ---- instrumentation (bench.py, profiling) ------------------------------ */
+/* With non-NULL cudaEvent_t handles, every subsequent device call records
+ * `start` right before and `stop` right after its stage-1 streaming kernel,
+ * on that call's stream (the dominant kernel's live duration).  NULL, NULL
+ * disables.  Process-wide; not for concurrent use. */
+void atkg_set_profile_events(void* start, void* stop);
+/* Kernels launched by this library so far (process-wide counter). */
+uint64_t atkg_launch_count(void);
 
 #ifdef __cplusplus
 }

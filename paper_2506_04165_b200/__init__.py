@@ -9,7 +9,7 @@ from ._lib import NoFeasibleConfigError  # noqa: F401
 from .planner import (PlanRequest, PlanResult, RecallEstimate, exact_expected_recall,  # noqa: F401
                       legal_bucket_counts, mc_expected_recall, mc_expected_recall_adaptive,
                       select_parameters)
-from .topk import (AlgoParams, Stage1Accumulator, TopKResult, approx_top_k, approx_top_k_batch,  # noqa: F401
+from .topk import (AlgoParams, Stage1Accumulator, TopKResult, approx_top_k, approx_top_k_batch, check_status,  # noqa: F401
                    approx_top_k_device, exact_top_k, exact_top_k_device, kDefaultLaneMultiple, kNegInf,
                    measure_recall, partition_index, select_candidates_device, select_top_k_candidates,
                    stage1_device, stage1_partial_reduce, stage1_summary_device, summary_merge_top_k_device,

@@ -43,7 +43,7 @@ class PlanResultC(C.Structure):
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2506_04165_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2506_04165_b200/build.py` "
             "(there is no CPU fallback)")
     lib = C.CDLL(LIB_PATH)
     P = C.POINTER(Params)
@@ -52,6 +52,7 @@ def _load():
     sigs = {
         "atkg_last_error": ([], C.c_char_p),
         "atkg_version": ([], C.c_char_p),
+        "atkg_set_device": ([i32], i32),
         "atkg_validate": ([P], i32),
         "atkg_validate_analysis": ([P], i32),
         "atkg_workspace_size": ([i32, i32, u64, P, sz], i32),
@@ -83,6 +84,8 @@ def _load():
         "atkg_fill_normal": ([u64, u64, C.c_float, C.c_float, vp, u32], None),
         "atkg_f32_to_bf16": ([vp, u64, vp, u32], None),
         "atkg_bf16_to_f32": ([vp, u64, vp, u32], None),
+        "atkg_set_profile_events": ([vp, vp], None),
+        "atkg_launch_count": ([], u64),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)

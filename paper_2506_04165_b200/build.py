@@ -1,6 +1,6 @@
 """Builds paper_2506_04165_b200/libatkg.so (the C-ABI library) for sm_100a.
 
-    python -m paper_2506_04165_b200.build [--force] [-j N]
+    python paper_2506_04165_b200/build.py [--force] [-j N]
 
 Every .cu/.cpp under csrc/ is compiled with nvcc
 (-gencode arch=compute_100a,code=sm_100a -lineinfo -O3) into build/ and linked

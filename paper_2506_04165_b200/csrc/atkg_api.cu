@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -27,7 +28,13 @@ void set_last_error(const std::string& m) { g_last_error = m; }
     if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-inline void check_launch() { CUDA_OK(cudaGetLastError()); }
+std::atomic<uint64_t> g_launches{0};
+cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
+
+inline void check_launch() {
+  CUDA_OK(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
 
 constexpr int kSegWarps = 8;   // warps (= segments) per stage-1 CTA
 constexpr int kPrefetch = 4;   // stride-rows per batch in the stage-1 loop
@@ -72,10 +79,10 @@ bool kp_specialised(uint32_t kp) { return (kp >= 1 && kp <= 8) || kp == 16; }
 struct S1Plan {
   bool generic = false;
   int V = 4;
-  uint32_t tiles = 0, segs = 0, cpr = 0;
+  uint32_t tiles = 0, segs = 0, cpr = 0, group = 1;
+  uint64_t groups = 0;
   uint64_t seg_len = 0, nstr = 0;
   size_t smem = 0;
-  uint64_t summary_words() const { return 0; }
 };
 
 S1Plan plan_stage1(int dtype, const void* in, uint64_t rows, uint64_t len, uint64_t row_stride,
@@ -99,8 +106,11 @@ S1Plan plan_stage1(int dtype, const void* in, uint64_t rows, uint64_t len, uint6
   pl.seg_len = std::max<uint64_t>(1, ceil_div(pl.nstr, segs));
   if (pl.nstr >= kp) pl.seg_len = std::max<uint64_t>(pl.seg_len, kp);
   pl.segs = static_cast<uint32_t>(std::max<uint64_t>(1, ceil_div(pl.nstr, pl.seg_len)));
-  pl.cpr = static_cast<uint32_t>(ceil_div(pl.segs, kSegWarps));
-  pl.smem = static_cast<size_t>(kSegWarps / 2) * (2 * kp + 2) * V * 32 * 4;
+  pl.group = 1;
+  while (pl.group < kSegWarps && pl.group < pl.segs) pl.group <<= 1;
+  pl.cpr = static_cast<uint32_t>(ceil_div(pl.segs, pl.group));
+  pl.groups = rows * pl.tiles * pl.cpr;
+  pl.smem = pl.group > 1 ? static_cast<size_t>(kSegWarps / 2) * (2 * kp + 2) * V * 32 * 4 : 0;
   return pl;
 }
 
@@ -112,9 +122,11 @@ void launch_segments(const S1Plan& pl, const SegArgs& a, cudaStream_t st) {
     CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr = true;
   }
-  const uint64_t grid = a.rows * pl.tiles * pl.cpr;
+  const uint64_t grid = ceil_div(pl.groups, kSegWarps / pl.group);
+  if (g_prof_start) CUDA_OK(cudaEventRecord(g_prof_start, st));
   kern<<<static_cast<unsigned>(grid), kSegWarps * 32, pl.smem, st>>>(a);
   check_launch();
+  if (g_prof_stop) CUDA_OK(cudaEventRecord(g_prof_stop, st));
 }
 
 template <typename T>
@@ -192,6 +204,8 @@ void run_stage1_grid(int dtype, const void* in, uint64_t rows, const atkg_params
   a.seg_len = pl.seg_len;
   a.segs = pl.segs;
   a.cta_per_row_tile = pl.cpr;
+  a.group = pl.group;
+  a.groups = pl.groups;
   a.tiles = pl.tiles;
   a.out = static_cast<uint32_t*>(ws);
   a.status = status;
@@ -316,6 +330,17 @@ extern "C" {
 
 const char* atkg_last_error(void) { return g_last_error.c_str(); }
 const char* atkg_version(void) { return "atkg 0.1 (sm_100a)"; }
+
+int atkg_set_device(int device) {
+  return guarded([&] { CUDA_OK(cudaSetDevice(device)); });
+}
+
+void atkg_set_profile_events(void* start, void* stop) {
+  g_prof_start = static_cast<cudaEvent_t>(start);
+  g_prof_stop = static_cast<cudaEvent_t>(stop);
+}
+
+uint64_t atkg_launch_count(void) { return g_launches.load(); }
 
 int atkg_validate(const atkg_params* p) {
   return guarded([&] { validate(*p); });
@@ -447,6 +472,8 @@ int atkg_stage1_summary(int dtype, const void* d_slice, uint64_t len, uint64_t i
     a.seg_len = pl.seg_len;
     a.segs = pl.segs;
     a.cta_per_row_tile = pl.cpr;
+    a.group = pl.group;
+    a.groups = pl.groups;
     a.tiles = pl.tiles;
     a.out = reinterpret_cast<uint32_t*>(w);
     a.status = d_status;
@@ -735,6 +762,8 @@ int atkg_accumulator_consume(atkg_accumulator* a, int dtype, const void* d_block
         s.seg_len = pl.seg_len;
         s.segs = pl.segs;
         s.cta_per_row_tile = pl.cpr;
+        s.group = pl.group;
+        s.groups = pl.groups;
         s.tiles = pl.tiles;
         s.out = static_cast<uint32_t*>(a->ws);
         s.status = a->status;

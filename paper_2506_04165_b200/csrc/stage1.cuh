@@ -223,9 +223,12 @@ struct SegArgs {
   uint64_t index_offset; // position of the first element (slice sharding)
   uint64_t seg_len;      // stride-rows per segment (>= KP unless nstr < KP)
   uint32_t segs;         // segments per row
-  uint32_t cta_per_row_tile;  // ceil(segs / W)
+  uint32_t cta_per_row_tile;  // summary blocks per (row, tile) = ceil(segs / G)
+  uint32_t group;        // G: warps that cooperate on one (row, tile), power of 2 <= W
+  uint64_t groups;       // rows * tiles * cta_per_row_tile
   uint32_t tiles;        // ceil(B / (32 V))
   uint32_t* out;         // summary blocks [rows][cta_per_row_tile][words]
+                         // (W/G groups per CTA; group = G consecutive segments)
   uint32_t* status;
 };
 
@@ -262,14 +265,17 @@ stage1_segments_kernel(SegArgs a) {
   extern __shared__ uint32_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  uint64_t blk = blockIdx.x;
-  const uint32_t cseg = (uint32_t)(blk % a.cta_per_row_tile);
-  blk /= a.cta_per_row_tile;
-  const uint32_t tile = (uint32_t)(blk % a.tiles);
-  const uint64_t row = blk / a.tiles;
+  const uint32_t G = a.group;
+  const int gw = warp & (G - 1);  // warp within its group
+  uint64_t grp = (uint64_t)blockIdx.x * (W / G) + warp / G;
+  const bool grp_ok = grp < a.groups;
+  const uint32_t cseg = (uint32_t)(grp % a.cta_per_row_tile);
+  grp /= a.cta_per_row_tile;
+  const uint32_t tile = (uint32_t)(grp % a.tiles);
+  const uint64_t row = grp / a.tiles;
   const uint64_t b0 = ((uint64_t)tile * 32 + lane) * V;  // first bucket of this lane
-  const bool lane_ok = b0 < a.B;
-  const uint32_t seg = cseg * W + warp;
+  const bool lane_ok = grp_ok && b0 < a.B;
+  const uint32_t seg = cseg * G + gw;
 
   Summ<KP> s[V];
 #pragma unroll
@@ -328,14 +334,15 @@ stage1_segments_kernel(SegArgs a) {
   }
   if (nan) atomicOr(a.status, ATKG_FLAG_NAN);
 
-  // CTA tree merge: after the step, warp w (w % 2step == 0) holds the merge
-  // of warps [w, w + 2 step)
+  // group tree merge: after the step, warp gw (gw % 2step == 0) holds the
+  // merge of the group's warps [gw, gw + 2 step)
   constexpr int kWords = (2 * KP + 2) * V * 32;
 #pragma unroll
   for (int step = 1; step < W; step *= 2) {
-    if ((warp % (2 * step)) == step) smem_put<KP, V>(smem + (warp / (2 * step)) * kWords, lane, s);
+    if (step >= (int)G) break;  // uniform across the CTA
+    if ((gw % (2 * step)) == step) smem_put<KP, V>(smem + (warp / (2 * step)) * kWords, lane, s);
     __syncthreads();
-    if ((warp % (2 * step)) == 0 && warp + step < W) {
+    if ((gw % (2 * step)) == 0 && gw + step < (int)G) {
       Summ<KP> o[V];
       smem_get<KP, V>(smem + (warp / (2 * step)) * kWords, lane, o);
 #pragma unroll
@@ -343,7 +350,7 @@ stage1_segments_kernel(SegArgs a) {
     }
     __syncthreads();
   }
-  if (warp == 0 && lane_ok) {
+  if (gw == 0 && lane_ok) {
     const uint64_t words = (uint64_t)(2 * KP + 2) * a.B;
     uint32_t* dst = a.out + (row * a.cta_per_row_tile + cseg) * words;
 #pragma unroll

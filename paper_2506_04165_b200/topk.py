@@ -119,7 +119,16 @@ def workspace(nbytes: int, device) -> "torch.Tensor":
     return buf
 
 
+_cur_dev = [None]
+
+
 def _stream_ptr(device) -> int:
+    """Current torch stream of `device`; also points the library's CUDA
+    runtime at that device (it keeps its own per-thread device state)."""
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    if _cur_dev[0] != idx:
+        check(lib.atkg_set_device(idx))
+        _cur_dev[0] = idx
     return torch.cuda.current_stream(device).cuda_stream
 
 
