@@ -232,11 +232,13 @@ void atkg_f32_to_bf16(const float* in, uint64_t count, uint16_t* out, uint32_t t
 void atkg_bf16_to_f32(const uint16_t* in, uint64_t count, float* out, uint32_t threads);
 
 /* ---- instrumentation (bench.py, profiling) ------------------------------ */
-/* With non-NULL cudaEvent_t handles, every subsequent device call records
- * `start` right before and `stop` right after its stage-1 streaming kernel,
- * on that call's stream (the dominant kernel's live duration).  NULL, NULL
- * disables.  Process-wide; not for concurrent use. */
-void atkg_set_profile_events(void* start, void* stop);
+/* Between atkg_profile_begin() and atkg_profile_end(), every stage-1
+ * streaming kernel (the dominant kernel) launched by this library is
+ * bracketed by CUDA events on its own stream; profile_end synchronises and
+ * returns the summed device duration and the number of such launches.
+ * Process-wide; not for concurrent use. */
+void atkg_profile_begin(void);
+int atkg_profile_end(double* total_ms, uint64_t* launches);
 /* Kernels launched by this library so far (process-wide counter). */
 uint64_t atkg_launch_count(void);
 

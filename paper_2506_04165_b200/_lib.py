@@ -84,7 +84,8 @@ def _load():
         "atkg_fill_normal": ([u64, u64, C.c_float, C.c_float, vp, u32], None),
         "atkg_f32_to_bf16": ([vp, u64, vp, u32], None),
         "atkg_bf16_to_f32": ([vp, u64, vp, u32], None),
-        "atkg_set_profile_events": ([vp, vp], None),
+        "atkg_profile_begin": ([], None),
+        "atkg_profile_end": ([f64p, C.POINTER(C.c_uint64)], i32),
         "atkg_launch_count": ([], u64),
     }
     for name, (args, res) in sigs.items():

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -29,7 +30,28 @@ void set_last_error(const std::string& m) { g_last_error = m; }
   } while (0)
 
 std::atomic<uint64_t> g_launches{0};
-cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // pairs
+  size_t used = 0;
+  void bracket_begin(cudaStream_t st) {
+    if (!on) return;
+    if (used + 2 > ev.size()) {
+      for (int q = 0; q < 2; ++q) {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreate(&e));
+        ev.push_back(e);
+      }
+    }
+    CUDA_OK(cudaEventRecord(ev[used], st));
+  }
+  void bracket_end(cudaStream_t st) {
+    if (!on) return;
+    CUDA_OK(cudaEventRecord(ev[used + 1], st));
+    used += 2;
+  }
+};
+Profiler g_prof;
 
 inline void check_launch() {
   CUDA_OK(cudaGetLastError());
@@ -78,55 +100,145 @@ bool kp_specialised(uint32_t kp) { return (kp >= 1 && kp <= 8) || kp == 16; }
 // ---------------------------------------------------------------------------
 struct S1Plan {
   bool generic = false;
+  bool stream = false;  // TMA-fed streaming kernel
   int V = 4;
   uint32_t tiles = 0, segs = 0, cpr = 0, group = 1;
+  int warps = 8;
   uint64_t groups = 0;
   uint64_t seg_len = 0, nstr = 0;
   size_t smem = 0;
 };
 
+constexpr int kStreamSlots = 4;   // TMA ring slots per warp
+constexpr int kStreamRows = 8;    // stride-rows per ring slot
+constexpr int kStreamWarps = 4;   // warps per streaming CTA
+constexpr int kLogCap = 16;       // log entries per (lane, bucket)
+// lanes own V adjacent buckets; fewer for long lists to bound registers
+constexpr int stream_vec(int kp) { return kp <= 4 ? 4 : (kp <= 8 ? 2 : 1); }
+// stride-rows each warp samples for the group threshold
+constexpr int stream_q0(int kp) { return kp <= 2 ? 8 : 4 * kp; }
+
+template <typename T, int KP>
+const void* stream_kernel_ptr() {
+  return reinterpret_cast<const void*>(
+      stage1_stream_kernel<T, KP, stream_vec(KP), kStreamWarps, kStreamSlots, kStreamRows, kLogCap, stream_q0(KP)>);
+}
+template <typename T, int KP>
+constexpr size_t stream_smem() {
+  return stream_smem_bytes<T, KP, stream_vec(KP), kStreamWarps, kStreamSlots, kStreamRows, kLogCap>();
+}
+int stream_ctas_per_sm(int dtype, uint32_t kp);
+
+uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::strtoull(e, nullptr, 10) : dflt;
+}
+
 S1Plan plan_stage1(int dtype, const void* in, uint64_t rows, uint64_t len, uint64_t row_stride,
                    uint64_t B, uint32_t kp) {
   S1Plan pl;
   const int esz = dtype == ATKG_BF16 ? 2 : 4;
-  const int V = 4;
-  const bool aligned = (reinterpret_cast<uintptr_t>(in) % (V * esz) == 0) && (row_stride % V == 0);
-  if (!kp_specialised(kp) || B % V != 0 || !aligned) {
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(in);
+  const bool aligned = (addr % (4 * esz) == 0) && (row_stride % 4 == 0);
+  if (!kp_specialised(kp) || B % 4 != 0 || !aligned) {
     pl.generic = true;
     return pl;
   }
-  pl.V = V;
   pl.nstr = len / B;
+  const int V = stream_vec(kp);
+  // 1-D TMA needs 16-byte aligned rows and copy sizes
+  pl.stream = (addr % 16 == 0) && ((row_stride * esz) % 16 == 0) && ((B * esz) % 16 == 0) && (B % V == 0) &&
+              env_u64("ATKG_NO_STREAM", 0) == 0;
+  pl.V = V;
   pl.tiles = static_cast<uint32_t>(ceil_div(B, 32ull * V));
   const uint64_t units = rows * pl.tiles;
-  const uint64_t target_warps = static_cast<uint64_t>(sm_count()) * 32;
-  const uint64_t min_len = std::max<uint64_t>(kp, 32);
-  uint64_t max_segs = std::max<uint64_t>(1, pl.nstr / min_len);
-  uint64_t segs = std::min<uint64_t>(max_segs, std::max<uint64_t>(1, ceil_div(target_warps, units)));
-  pl.seg_len = std::max<uint64_t>(1, ceil_div(pl.nstr, segs));
+  uint64_t segs;
+  if (pl.stream) {
+    const uint64_t target = static_cast<uint64_t>(sm_count()) * stream_ctas_per_sm(dtype, kp) * kStreamWarps;
+    const uint64_t min_len = std::max<uint64_t>(kp, kStreamRows);
+    const uint64_t max_segs = std::max<uint64_t>(1, pl.nstr / min_len);
+    segs = std::min<uint64_t>(max_segs, std::max<uint64_t>(1, target / std::max<uint64_t>(1, units)));
+    // whole groups: a power of two below the CTA width, else a multiple of it
+    if (segs >= (uint64_t)kStreamWarps) segs = segs / kStreamWarps * kStreamWarps;
+    else while (segs & (segs - 1)) segs &= segs - 1;
+    segs = env_u64("ATKG_SEGS", segs);
+    pl.seg_len = std::max<uint64_t>(1, ceil_div(ceil_div(pl.nstr, segs), kStreamRows) * kStreamRows);
+    pl.seg_len = std::min<uint64_t>(pl.seg_len, 65536);  // log rows are 16-bit offsets
+  } else {
+    const uint64_t target_warps = static_cast<uint64_t>(sm_count()) * 32;
+    const uint64_t min_len = std::max<uint64_t>(kp, 32);
+    const uint64_t max_segs = std::max<uint64_t>(1, pl.nstr / min_len);
+    segs = std::min<uint64_t>(max_segs, std::max<uint64_t>(1, ceil_div(target_warps, units)));
+    pl.seg_len = std::max<uint64_t>(1, ceil_div(pl.nstr, segs));
+  }
   if (pl.nstr >= kp) pl.seg_len = std::max<uint64_t>(pl.seg_len, kp);
   pl.segs = static_cast<uint32_t>(std::max<uint64_t>(1, ceil_div(pl.nstr, pl.seg_len)));
+  pl.warps = pl.stream ? kStreamWarps : kSegWarps;
   pl.group = 1;
-  while (pl.group < kSegWarps && pl.group < pl.segs) pl.group <<= 1;
+  while (pl.group < (uint32_t)pl.warps && pl.group < pl.segs) pl.group <<= 1;
   pl.cpr = static_cast<uint32_t>(ceil_div(pl.segs, pl.group));
   pl.groups = rows * pl.tiles * pl.cpr;
   pl.smem = pl.group > 1 ? static_cast<size_t>(kSegWarps / 2) * (2 * kp + 2) * V * 32 * 4 : 0;
   return pl;
 }
 
+template <typename T>
+int stream_occupancy(uint32_t kp) {
+  const void* k = nullptr;
+  size_t smem = 0;
+  switch (kp) {
+#define ATKG_OCC(K) case K: k = stream_kernel_ptr<T, K>(); smem = stream_smem<T, K>(); break;
+    ATKG_OCC(1) ATKG_OCC(2) ATKG_OCC(3) ATKG_OCC(4) ATKG_OCC(5) ATKG_OCC(6) ATKG_OCC(7) ATKG_OCC(8) ATKG_OCC(16)
+#undef ATKG_OCC
+    default: return 1;
+  }
+  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int n = 0;
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kStreamWarps * 32, smem));
+  return n > 0 ? n : 1;
+}
+
+int stream_ctas_per_sm(int dtype, uint32_t kp) {
+  static int cache[2][17] = {};
+  int& c = cache[dtype == ATKG_BF16 ? 1 : 0][kp <= 16 ? kp : 0];
+  if (c == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+    int cc = 0;
+    cudaDeviceGetAttribute(&cc, cudaDevAttrComputeCapabilityMajor, dev);
+    if (cc < 10) return 1;  // planning without an sm_100 device (workspace sizing)
+    c = dtype == ATKG_BF16 ? stream_occupancy<__nv_bfloat16>(kp) : stream_occupancy<float>(kp);
+  }
+  return c;
+}
+
 template <typename T, int KP>
 void launch_segments(const S1Plan& pl, const SegArgs& a, cudaStream_t st) {
+  const uint64_t grid = ceil_div(pl.groups, pl.warps / pl.group);
+  if (pl.stream) {
+    auto kern = stage1_stream_kernel<T, KP, stream_vec(KP), kStreamWarps, kStreamSlots, kStreamRows, kLogCap, stream_q0(KP)>;
+    constexpr size_t smem = stream_smem<T, KP>();
+    static bool attr = false;
+    if (!attr) {
+      CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    g_prof.bracket_begin(st);
+    kern<<<static_cast<unsigned>(grid), kStreamWarps * 32, smem, st>>>(a);
+    check_launch();
+    g_prof.bracket_end(st);
+    return;
+  }
   auto kern = stage1_segments_kernel<T, KP, 4, kSegWarps, kPrefetch>;
   static bool attr = false;
   if (!attr) {
     CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr = true;
   }
-  const uint64_t grid = ceil_div(pl.groups, kSegWarps / pl.group);
-  if (g_prof_start) CUDA_OK(cudaEventRecord(g_prof_start, st));
+  g_prof.bracket_begin(st);
   kern<<<static_cast<unsigned>(grid), kSegWarps * 32, pl.smem, st>>>(a);
   check_launch();
-  if (g_prof_stop) CUDA_OK(cudaEventRecord(g_prof_stop, st));
+  g_prof.bracket_end(st);
 }
 
 template <typename T>
@@ -335,9 +447,24 @@ int atkg_set_device(int device) {
   return guarded([&] { CUDA_OK(cudaSetDevice(device)); });
 }
 
-void atkg_set_profile_events(void* start, void* stop) {
-  g_prof_start = static_cast<cudaEvent_t>(start);
-  g_prof_stop = static_cast<cudaEvent_t>(stop);
+void atkg_profile_begin(void) {
+  g_prof.on = true;
+  g_prof.used = 0;
+}
+
+int atkg_profile_end(double* total_ms, uint64_t* launches) {
+  return guarded([&] {
+    g_prof.on = false;
+    double sum = 0.0;
+    for (size_t q = 0; q < g_prof.used; q += 2) {
+      CUDA_OK(cudaEventSynchronize(g_prof.ev[q + 1]));
+      float ms = 0.f;
+      CUDA_OK(cudaEventElapsedTime(&ms, g_prof.ev[q], g_prof.ev[q + 1]));
+      sum += ms;
+    }
+    *total_ms = sum;
+    *launches = g_prof.used / 2;
+  });
 }
 
 uint64_t atkg_launch_count(void) { return g_launches.load(); }

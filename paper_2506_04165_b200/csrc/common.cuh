@@ -17,6 +17,7 @@ constexpr uint32_t kEmptyPos = 0xffffffffu;  // unfilled summary slot / "none"
 
 ATKG_HD float neg_inf() { return -INFINITY; }
 ATKG_HD uint32_t umax32(uint32_t a, uint32_t b) { return a > b ? a : b; }
+ATKG_HD uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
 // Sortable 64-bit rank key (src/topk.cpp:30-39): high 32 bits order by value
 // descending over the IEEE total order with -0.0 canonicalised to +0.0, low

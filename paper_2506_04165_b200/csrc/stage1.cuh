@@ -26,6 +26,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace atkg {
 
@@ -259,6 +260,36 @@ __device__ __forceinline__ void smem_get(const uint32_t* sm, int lane, Summ<KP> 
   }
 }
 
+// group tree merge: after the step, warp gw (gw % 2step == 0) holds the
+// merge of its group's warps [gw, gw + 2 step); warp 0 of the group writes
+// the group's summary block.
+template <int KP, int V, int W>
+__device__ __forceinline__ void group_merge_store(uint32_t* smem, int warp, int lane, int gw, uint32_t G,
+                                                  bool lane_ok, uint64_t row, uint32_t cseg, uint64_t b0,
+                                                  const SegArgs& a, Summ<KP> (&s)[V]) {
+  constexpr int kWords = (2 * KP + 2) * V * 32;
+#pragma unroll
+  for (int step = 1; step < W; step *= 2) {
+    if (step >= (int)G) break;  // uniform across the CTA
+    if ((gw % (2 * step)) == step) smem_put<KP, V>(smem + (warp / (2 * step)) * kWords, lane, s);
+    __syncthreads();
+    if ((gw % (2 * step)) == 0 && gw + step < (int)G) {
+      Summ<KP> o[V];
+      smem_get<KP, V>(smem + (warp / (2 * step)) * kWords, lane, o);
+#pragma unroll
+      for (int v = 0; v < V; ++v) s[v].merge_later(o[v]);
+    }
+    __syncthreads();
+  }
+  if (gw == 0 && lane_ok) {
+    const uint64_t words = (uint64_t)(2 * KP + 2) * a.B;
+    uint32_t* dst = a.out + (row * a.cta_per_row_tile + cseg) * words;
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (b0 + v < a.B) store_summ<KP>(dst, a.B, b0 + v, s[v]);
+  }
+}
+
 template <typename T, int KP, int V, int W, int D>
 __global__ void __launch_bounds__(W * 32)
 stage1_segments_kernel(SegArgs a) {
@@ -334,29 +365,7 @@ stage1_segments_kernel(SegArgs a) {
   }
   if (nan) atomicOr(a.status, ATKG_FLAG_NAN);
 
-  // group tree merge: after the step, warp gw (gw % 2step == 0) holds the
-  // merge of the group's warps [gw, gw + 2 step)
-  constexpr int kWords = (2 * KP + 2) * V * 32;
-#pragma unroll
-  for (int step = 1; step < W; step *= 2) {
-    if (step >= (int)G) break;  // uniform across the CTA
-    if ((gw % (2 * step)) == step) smem_put<KP, V>(smem + (warp / (2 * step)) * kWords, lane, s);
-    __syncthreads();
-    if ((gw % (2 * step)) == 0 && gw + step < (int)G) {
-      Summ<KP> o[V];
-      smem_get<KP, V>(smem + (warp / (2 * step)) * kWords, lane, o);
-#pragma unroll
-      for (int v = 0; v < V; ++v) s[v].merge_later(o[v]);
-    }
-    __syncthreads();
-  }
-  if (gw == 0 && lane_ok) {
-    const uint64_t words = (uint64_t)(2 * KP + 2) * a.B;
-    uint32_t* dst = a.out + (row * a.cta_per_row_tile + cseg) * words;
-#pragma unroll
-    for (int v = 0; v < V; ++v)
-      if (b0 + v < a.B) store_summ<KP>(dst, a.B, b0 + v, s[v]);
-  }
+  group_merge_store<KP, V, W>(smem, warp, lane, gw, G, lane_ok, row, cseg, b0, a, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -495,6 +504,283 @@ __global__ void fold_grid_kernel(float* gv, uint32_t* gi, uint64_t B, uint32_t k
 __global__ void grid_init_kernel(float* gv, uint32_t* gi, uint64_t count) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < count) { gv[t] = neg_inf(); gi[t] = 0; }
+}
+
+}  // namespace atkg
+
+// ---------------------------------------------------------------------------
+// TMA-fed streaming kernel (the hot path).  Every warp streams one long
+// segment of one (row, 32*V-bucket tile) through its own ring of NS shared-
+// memory slots filled by 1-D bulk copies (cp.async.bulk -> UBLKCP), so
+// memory-level parallelism comes from the ring depth, not from thread count,
+// and segments can be long -- long segments keep the Alg. 1 insert rate (and
+// with it the divergent slow path) low.  Lane l owns buckets tile*32V + l*V
+// .. +V-1 and reads its V elements of every stride-row from shared memory.
+// ---------------------------------------------------------------------------
+
+namespace atkg {
+
+template <typename T, int V>
+__device__ __forceinline__ void lds_vec(const uint8_t* p, float (&out)[V]) {
+  constexpr int kBytes = sizeof(T) * V;
+  uint32_t w[(kBytes + 3) / 4];
+  if constexpr (kBytes == 16) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    w[0] = u.x; w[1] = u.y; w[2] = u.z; w[3] = u.w;
+  } else if constexpr (kBytes == 8) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    w[0] = u.x; w[1] = u.y;
+  } else {
+    w[0] = *reinterpret_cast<const uint32_t*>(p);
+  }
+  VecLoad<T, V>::unpack(w, out);
+}
+
+// Hot loop = filter -> log -> flush.  Per element the common path is one
+// compare against a per-bucket threshold f plus a predicated append to a
+// per-lane log in shared memory -- 4 instructions, no branch, full SIMT
+// width.  f never exceeds the exact current K'-th value of the bucket (it is
+// refreshed at every flush), so the log holds every element the sequential
+// algorithm would send down its slow path (plus some it rejects on replay).
+// A flush replays each lane's logs in index order through the exact summary
+// update (Summ::push), warp-synchronously, then raises f.
+// Loads are 128-bit (V elements per lane), D stride-rows per block with the
+// next block prefetched into registers while the current one is filtered.
+// Log layout per warp (structure of arrays, lane-minor, conflict-free):
+//   float    val[V][LOGC][32]   element value
+//   uint16_t row[V][LOGC][32]   stride-row offset j - j0 of the element
+__device__ __forceinline__ void log_append(uint32_t& pv, uint32_t& pj, float x, float f, uint16_t jrel) {
+  // appends (x, jrel) when !(x < f) -- NaN included -- and bumps both cursors
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.geu.f32 p, %2, %3;\n\t"
+      "@p st.shared.f32 [%0], %2;\n\t"
+      "@p st.shared.u16 [%1], %4;\n\t"
+      "@p add.u32 %0, %0, 128;\n\t"
+      "@p add.u32 %1, %1, 64;\n\t}"
+      : "+r"(pv), "+r"(pj)
+      : "f"(x), "f"(f), "h"(jrel)
+      : "memory");
+}
+
+template <typename T, int KP, int V, int W, int NS, int CR, int LOGC, int Q0>
+__global__ void __launch_bounds__(W * 32)
+stage1_stream_kernel(SegArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  static_assert(LOGC >= 2 * CR, "log must absorb a chunk between flush checks");
+  constexpr int LB = V * sizeof(T);              // bytes per lane per stride-row
+  constexpr int SB = CR * 32 * LB;               // bytes per ring slot
+  constexpr int RING = NS * SB;
+  constexpr int LOGV = V * LOGC * 32;            // log entries per warp
+  constexpr int WARP_BYTES = RING + LOGV * 6;    // ring + val[] + row[]
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  uint8_t* ring = smem_raw + warp * WARP_BYTES;
+  uint8_t* lbase = ring + RING;
+  const float* logv = reinterpret_cast<const float*>(lbase);
+  const uint16_t* logj = reinterpret_cast<const uint16_t*>(lbase + LOGV * 4);
+  const uint32_t sv0 = (uint32_t)__cvta_generic_to_shared(lbase) + lane * 4;
+  const uint32_t sj0 = (uint32_t)__cvta_generic_to_shared(lbase + LOGV * 4) + lane * 2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + W * WARP_BYTES) + warp * NS;
+
+  const uint32_t G = a.group;
+  const int gw = warp & (G - 1);
+  uint64_t grp = (uint64_t)blockIdx.x * (W / G) + warp / G;
+  const bool grp_ok = grp < a.groups;
+  const uint32_t cseg = (uint32_t)(grp % a.cta_per_row_tile);
+  grp /= a.cta_per_row_tile;
+  const uint32_t tile = (uint32_t)(grp % a.tiles);
+  const uint64_t row = grp / a.tiles;
+  const uint64_t tb0 = (uint64_t)tile * 32 * V;
+  const uint64_t b0 = tb0 + (uint64_t)lane * V;
+  const bool lane_ok = grp_ok && b0 < a.B;
+  const uint32_t seg = cseg * G + gw;
+  const uint64_t B = a.B;
+  const uint64_t j0 = (uint64_t)seg * a.seg_len;
+  // trip counts are warp-uniform (warp-synchronous flushes); lanes past the
+  // last bucket read lane 0's data (real input, so a NaN there is a real
+  // NaN) and filter with f = +inf
+  const uint64_t j1 = (grp_ok && seg < a.segs) ? umin64(j0 + a.seg_len, a.nstr) : j0;
+  const uint32_t ioff = (uint32_t)(a.index_offset + b0);
+  const uint32_t Bu = (uint32_t)B;
+  const uint32_t tw = grp_ok ? (uint32_t)(umin64(32 * V, B - tb0) * sizeof(T)) : 0u;  // bytes per row
+  const bool contiguous = (a.tiles == 1) && ((uint64_t)tw == B * sizeof(T));
+  const uint32_t nch = (uint32_t)((j1 - j0 + CR - 1) / CR);
+  const char* gbase = reinterpret_cast<const char*>(a.in) + (row * a.row_stride + tb0) * sizeof(T);
+  const uint64_t gstride = B * sizeof(T);
+  const uint32_t lane_off = lane_ok ? lane * LB : 0u;
+
+  // ---- TMA ring: lane 0 keeps NS chunks of CR stride-rows in flight --------
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) ptx::mbar_init(&bars[q], 1);
+    ptx::fence_mbar_init();
+  }
+  __syncwarp();
+  const uint64_t pol = ptx::policy_evict_first();
+  auto issue = [&](uint32_t c) {
+    const uint32_t slot = c % NS;
+    const uint64_t jr = j0 + (uint64_t)c * CR;
+    const uint32_t rows = (uint32_t)umin64(CR, j1 - jr);
+    ptx::mbar_arrive_expect_tx(&bars[slot], rows * tw);
+    if (contiguous) {
+      ptx::bulk_g2s(ring + slot * SB, gbase + jr * gstride, rows * tw, &bars[slot], pol);
+    } else {
+      for (uint32_t r = 0; r < rows; ++r)
+        ptx::bulk_g2s(ring + slot * SB + r * tw, gbase + (jr + r) * gstride, tw, &bars[slot], pol);
+    }
+  };
+  if (lane == 0)
+    for (uint32_t c = 0; c < (nch < (uint32_t)NS ? nch : (uint32_t)NS); ++c) issue(c);
+
+  Summ<KP> s[V];
+  float f[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) { s[v].clear(); f[v] = neg_inf(); }
+  uint32_t nan = 0;
+
+  // ---- phase 0: threshold from a sample ------------------------------------
+  // Each warp takes the top-KP values (a sorting network on values only) of
+  // the first Q0 stride-rows of its segment; the warps of a group (same row
+  // and tile) pool them in shared memory and every bucket gets
+  // tau = KP-th largest of the pooled sample.  Any subset's KP-th value is a
+  // lower bound of the bucket's final KP-th value v*, and Alg. 1 over any
+  // subsequence that contains every element >= v* ends in the same state, so
+  // filtering with f >= tau from the first element on is exact -- and skips
+  // the cold start of every segment.  (The sample reads go through L2, where
+  // the ring's bulk copies of the same rows then hit.)
+  {
+    float net[V][KP];
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int k = 0; k < KP; ++k) net[v][k] = neg_inf();
+    const T* sbase = reinterpret_cast<const T*>(gbase + lane_off);
+    const uint64_t qend = umin64(j0 + Q0, j1);
+    for (uint64_t q = j0; q < qend; ++q) {
+      float x[V];
+      VecLoad<T, V>::load(sbase + q * B, x);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        float c = x[v];
+        if (c != c) c = neg_inf();  // NaN is caught by the filter below
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          const float hi = fmaxf(net[v][k], c);
+          c = fminf(net[v][k], c);
+          net[v][k] = hi;
+        }
+      }
+    }
+    // exchange area: the (still unused) log of every warp
+    float* mine = reinterpret_cast<float*>(lbase);
+#pragma unroll
+    for (int k = 0; k < KP; ++k)
+#pragma unroll
+      for (int v = 0; v < V; ++v) mine[(k * V + v) * 32 + lane] = net[v][k];
+    __syncthreads();
+    const int g0 = warp - gw;
+    for (int w2 = g0; w2 < g0 + (int)G; ++w2) {
+      if (w2 == warp) continue;
+      const float* other = reinterpret_cast<const float*>(smem_raw + w2 * WARP_BYTES + RING);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          float c = other[(k * V + v) * 32 + lane];
+#pragma unroll
+          for (int kk = 0; kk < KP; ++kk) {
+            const float hi = fmaxf(net[v][kk], c);
+            c = fminf(net[v][kk], c);
+            net[v][kk] = hi;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) f[v] = lane_ok ? net[v][KP - 1] : __int_as_float(0x7f800000);
+    __syncthreads();  // exchange area becomes the logs
+  }
+  float tau[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) tau[v] = f[v];
+
+  uint32_t ptr[V], pj[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) { ptr[v] = sv0 + v * LOGC * 128; pj[v] = sj0 + v * LOGC * 64; }
+
+  auto flush = [&]() {
+    uint32_t cnt[V], m = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      cnt[v] = (ptr[v] - (sv0 + v * LOGC * 128)) >> 7;
+      m = cnt[v] > m ? cnt[v] : m;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint32_t y = __shfl_xor_sync(0xffffffffu, m, o);
+      m = y > m ? y : m;
+    }
+    for (uint32_t e = 0; e < m; ++e) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if (e < cnt[v]) {
+          const float x = logv[(v * LOGC + e) * 32 + lane];
+          const uint32_t jj = (uint32_t)j0 + logj[(v * LOGC + e) * 32 + lane];
+          s[v].push(x, ioff + v + jj * Bu, nan);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      ptr[v] = sv0 + v * LOGC * 128;
+      pj[v] = sj0 + v * LOGC * 64;
+      f[v] = s[v].full() ? fmaxf(s[v].v[KP - 1], tau[v]) : tau[v];
+    }
+  };
+
+  for (uint32_t c = 0; c < nch; ++c) {
+    const uint32_t slot = c % NS;
+    ptx::mbar_wait(&bars[slot], (c / NS) & 1u);
+    const uint32_t jrel0 = c * CR;
+    const uint32_t rows = (uint32_t)umin64(CR, j1 - (j0 + jrel0));
+    const uint8_t* sl = ring + slot * SB + lane_off;
+    if (rows == CR) {
+#pragma unroll
+      for (int r = 0; r < CR; ++r) {
+        float x[V];
+        lds_vec<T, V>(sl + r * tw, x);
+#pragma unroll
+        for (int v = 0; v < V; ++v) log_append(ptr[v], pj[v], x[v], f[v], (uint16_t)(jrel0 + r));
+      }
+    } else {
+      for (uint32_t r = 0; r < rows; ++r) {
+        float x[V];
+        lds_vec<T, V>(sl + r * tw, x);
+#pragma unroll
+        for (int v = 0; v < V; ++v) log_append(ptr[v], pj[v], x[v], f[v], (uint16_t)(jrel0 + r));
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && c + NS < nch) issue(c + NS);
+    bool need = false;
+#pragma unroll
+    for (int v = 0; v < V; ++v) need |= ptr[v] > sv0 + (uint32_t)(v * LOGC + (LOGC - CR - 1)) * 128;
+    if (__any_sync(0xffffffffu, need)) flush();
+  }
+  flush();
+  if (nan) atomicOr(a.status, ATKG_FLAG_NAN);
+  __syncthreads();  // rings drained and logs done before the merge reuses smem
+  group_merge_store<KP, V, W>(reinterpret_cast<uint32_t*>(smem_raw), warp, lane, gw, G, lane_ok, row, cseg, b0,
+                              a, s);
+}
+
+template <typename T, int KP, int V, int W, int NS, int CR, int LOGC>
+constexpr size_t stream_smem_bytes() {
+  static_assert((size_t)KP * V * 32 * 4 <= (size_t)V * LOGC * 32 * 6, "sample must fit a warp's log area");
+  constexpr size_t work = (size_t)W * (NS * CR * 32 * V * sizeof(T) + V * LOGC * 32 * 6) + (size_t)W * NS * 8;
+  constexpr size_t merge = (size_t)(W / 2) * (2 * KP + 2) * V * 32 * 4;
+  return work > merge ? work : merge;
 }
 
 }  // namespace atkg

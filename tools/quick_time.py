@@ -14,7 +14,6 @@ def timeit(fn, iters=20, warm=3):
     e.record(); torch.cuda.synchronize()
     return s.elapsed_time(e) / iters
 
-dev = torch.device("cuda:0")
 cfgs = {
  "C1": (16, 32768, 512, 4, 128, "f32"),
  "C2": (256, 262144, 128, 2, 64, "f32"),
@@ -23,9 +22,14 @@ cfgs = {
  "C3k8": (8192, 14336, 128, 8, 287, "bf16"),
  "C5": (1, 1 << 30, 256, 8, 1024, "f32"),
 }
-which = sys.argv[1:] or list(cfgs)
-for name in which:
+def main():
+  which = sys.argv[1:] or list(cfgs)
+  for name in which:
+    _one(name)
+
+def _one(name):
     rows, n, B, kp, k, dt = cfgs[name]
+    dev = torch.device("cuda:0")
     if dt == "f32":
         x = torch.randn(rows, n, device=dev)
         esz = 4
@@ -43,3 +47,6 @@ for name in which:
     atk.check_status(st)
     del x
     torch.cuda.empty_cache()
+
+if __name__ == "__main__":
+    main()
