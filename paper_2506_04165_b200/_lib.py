@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libatkg.so")
+LIB_PATH = os.environ.get("ATKG_LIB") or os.path.join(_HERE, "libatkg.so")  # override: experiments only
 
 ATKG_OK, ATKG_EINVAL, ATKG_ENAN, ATKG_EINFEASIBLE, ATKG_ECUDA, ATKG_EUNSUPPORTED = range(6)
 ATKG_F32, ATKG_BF16 = 0, 1

@@ -21,8 +21,9 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(ROOT, "build", "atkg")
-LIB = os.path.join(PKG, "libatkg.so")
+BUILD = os.path.join(ROOT, "build", "atkg" + os.environ.get("ATKG_VARIANT_TAG", ""))
+LIB = os.environ.get("ATKG_BUILD_LIB") or os.path.join(PKG, "libatkg.so")
+EXTRA = os.environ.get("ATKG_DEFINES", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
@@ -46,7 +47,7 @@ def _compile(src: str, force: bool) -> tuple[str, str]:
         t = os.path.getmtime(obj)
         if t >= os.path.getmtime(src) and t >= _headers_mtime():
             return obj, ""
-    flags = CUFLAGS if src.endswith(".cu") else ARCH + CXXFLAGS
+    flags = (CUFLAGS if src.endswith(".cu") else ARCH + CXXFLAGS) + EXTRA
     cmd = [NVCC, *flags, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

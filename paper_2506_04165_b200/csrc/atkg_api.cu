@@ -97,138 +97,192 @@ bool kp_specialised(uint32_t kp) { return (kp >= 1 && kp <= 8) || kp == 16; }
 
 // ---------------------------------------------------------------------------
 // stage-1 launch plan
+//   flat     the balanced TMA-fed streaming kernel (stage1_flat_kernel) --
+//            the hot path; needs 16-byte aligned rows and copy sizes
+//   segments LDG fallback for 4-element-aligned inputs
+//   generic  one thread per bucket running Alg. 1 directly (any shape, any K')
+// Both summary paths leave `parts` summary blocks per row in the workspace,
+// folded by run_merge.
 // ---------------------------------------------------------------------------
-struct S1Plan {
-  bool generic = false;
-  bool stream = false;  // TMA-fed streaming kernel
-  int V = 4;
-  uint32_t tiles = 0, segs = 0, cpr = 0, group = 1;
-  int warps = 8;
-  uint64_t groups = 0;
-  uint64_t seg_len = 0, nstr = 0;
-  size_t smem = 0;
-};
-
-constexpr int kStreamSlots = 4;   // TMA ring slots per warp
-constexpr int kStreamRows = 8;    // stride-rows per ring slot
-constexpr int kStreamWarps = 4;   // warps per streaming CTA
-constexpr int kLogCap = 16;       // log entries per (lane, bucket)
+#ifndef ATKG_SLOTS
+#define ATKG_SLOTS 3
+#endif
+#ifndef ATKG_LOGC
+#define ATKG_LOGC 16
+#endif
+#ifndef ATKG_FLAT_W
+#define ATKG_FLAT_W 4
+#endif
+constexpr int kFlatSlots = ATKG_SLOTS;  // TMA ring slots per warp
+constexpr int kFlatRows = 8;            // stride-rows per ring slot
+constexpr int kFlatWarps = ATKG_FLAT_W; // warps per CTA (independent)
+constexpr int kLogCap = ATKG_LOGC;      // log entries per (lane, bucket)
 // lanes own V adjacent buckets; fewer for long lists to bound registers
-constexpr int stream_vec(int kp) { return kp <= 4 ? 4 : (kp <= 8 ? 2 : 1); }
-// stride-rows each warp samples for the group threshold
-constexpr int stream_q0(int kp) { return kp <= 2 ? 8 : 4 * kp; }
+// (at least 4 bytes per lane per row: the cp.async granule)
+#ifndef ATKG_FLAT_V4
+#define ATKG_FLAT_V4 4
+#endif
+constexpr int flat_vec(int kp, int esz = 4) {
+  const int v = kp <= 4 ? ATKG_FLAT_V4 : (kp <= 8 ? 2 : 1);
+  return v * esz >= 4 ? v : 4 / esz;
+}
+// stride-rows sampled for the starting threshold of every piece
+#ifndef ATKG_Q0
+#define ATKG_Q0 16
+#endif
+constexpr int flat_q0(int kp) { return kp <= 2 ? ATKG_Q0 : ATKG_Q0 / 2 * kp; }
 
 template <typename T, int KP>
-const void* stream_kernel_ptr() {
-  return reinterpret_cast<const void*>(
-      stage1_stream_kernel<T, KP, stream_vec(KP), kStreamWarps, kStreamSlots, kStreamRows, kLogCap, stream_q0(KP)>);
+auto flat_kernel_fn() {
+  return stage1_flat_kernel<T, KP, flat_vec(KP, sizeof(T)), kFlatWarps, kFlatSlots, kFlatRows, kLogCap, flat_q0(KP)>;
 }
 template <typename T, int KP>
-constexpr size_t stream_smem() {
-  return stream_smem_bytes<T, KP, stream_vec(KP), kStreamWarps, kStreamSlots, kStreamRows, kLogCap>();
+constexpr size_t flat_smem() {
+  return flat_smem_bytes<T, KP, flat_vec(KP, sizeof(T)), kFlatWarps, kFlatSlots, kFlatRows, kLogCap>();
 }
-int stream_ctas_per_sm(int dtype, uint32_t kp);
 
 uint64_t env_u64(const char* name, uint64_t dflt) {
   const char* e = std::getenv(name);
   return e ? std::strtoull(e, nullptr, 10) : dflt;
 }
 
-S1Plan plan_stage1(int dtype, const void* in, uint64_t rows, uint64_t len, uint64_t row_stride,
-                   uint64_t B, uint32_t kp) {
-  S1Plan pl;
-  const int esz = dtype == ATKG_BF16 ? 2 : 4;
-  const uintptr_t addr = reinterpret_cast<uintptr_t>(in);
-  const bool aligned = (addr % (4 * esz) == 0) && (row_stride % 4 == 0);
-  if (!kp_specialised(kp) || B % 4 != 0 || !aligned) {
-    pl.generic = true;
-    return pl;
-  }
-  pl.nstr = len / B;
-  const int V = stream_vec(kp);
-  // 1-D TMA needs 16-byte aligned rows and copy sizes
-  pl.stream = (addr % 16 == 0) && ((row_stride * esz) % 16 == 0) && ((B * esz) % 16 == 0) && (B % V == 0) &&
-              env_u64("ATKG_NO_STREAM", 0) == 0;
-  pl.V = V;
-  pl.tiles = static_cast<uint32_t>(ceil_div(B, 32ull * V));
-  const uint64_t units = rows * pl.tiles;
-  uint64_t segs;
-  if (pl.stream) {
-    const uint64_t target = static_cast<uint64_t>(sm_count()) * stream_ctas_per_sm(dtype, kp) * kStreamWarps;
-    const uint64_t min_len = std::max<uint64_t>(kp, kStreamRows);
-    const uint64_t max_segs = std::max<uint64_t>(1, pl.nstr / min_len);
-    segs = std::min<uint64_t>(max_segs, std::max<uint64_t>(1, target / std::max<uint64_t>(1, units)));
-    // whole groups: a power of two below the CTA width, else a multiple of it
-    if (segs >= (uint64_t)kStreamWarps) segs = segs / kStreamWarps * kStreamWarps;
-    else while (segs & (segs - 1)) segs &= segs - 1;
-    segs = env_u64("ATKG_SEGS", segs);
-    pl.seg_len = std::max<uint64_t>(1, ceil_div(ceil_div(pl.nstr, segs), kStreamRows) * kStreamRows);
-    pl.seg_len = std::min<uint64_t>(pl.seg_len, 65536);  // log rows are 16-bit offsets
-  } else {
-    const uint64_t target_warps = static_cast<uint64_t>(sm_count()) * 32;
-    const uint64_t min_len = std::max<uint64_t>(kp, 32);
-    const uint64_t max_segs = std::max<uint64_t>(1, pl.nstr / min_len);
-    segs = std::min<uint64_t>(max_segs, std::max<uint64_t>(1, ceil_div(target_warps, units)));
-    pl.seg_len = std::max<uint64_t>(1, ceil_div(pl.nstr, segs));
-  }
-  if (pl.nstr >= kp) pl.seg_len = std::max<uint64_t>(pl.seg_len, kp);
-  pl.segs = static_cast<uint32_t>(std::max<uint64_t>(1, ceil_div(pl.nstr, pl.seg_len)));
-  pl.warps = pl.stream ? kStreamWarps : kSegWarps;
-  pl.group = 1;
-  while (pl.group < (uint32_t)pl.warps && pl.group < pl.segs) pl.group <<= 1;
-  pl.cpr = static_cast<uint32_t>(ceil_div(pl.segs, pl.group));
-  pl.groups = rows * pl.tiles * pl.cpr;
-  pl.smem = pl.group > 1 ? static_cast<size_t>(kSegWarps / 2) * (2 * kp + 2) * V * 32 * 4 : 0;
-  return pl;
-}
-
 template <typename T>
-int stream_occupancy(uint32_t kp) {
+int flat_occupancy(uint32_t kp) {
   const void* k = nullptr;
   size_t smem = 0;
   switch (kp) {
-#define ATKG_OCC(K) case K: k = stream_kernel_ptr<T, K>(); smem = stream_smem<T, K>(); break;
+#define ATKG_OCC(K) case K: k = reinterpret_cast<const void*>(flat_kernel_fn<T, K>()); smem = flat_smem<T, K>(); break;
     ATKG_OCC(1) ATKG_OCC(2) ATKG_OCC(3) ATKG_OCC(4) ATKG_OCC(5) ATKG_OCC(6) ATKG_OCC(7) ATKG_OCC(8) ATKG_OCC(16)
 #undef ATKG_OCC
     default: return 1;
   }
   CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int n = 0;
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kStreamWarps * 32, smem));
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kFlatWarps * 32, smem));
   return n > 0 ? n : 1;
 }
 
-int stream_ctas_per_sm(int dtype, uint32_t kp) {
+int flat_ctas_per_sm(int dtype, uint32_t kp) {
   static int cache[2][17] = {};
   int& c = cache[dtype == ATKG_BF16 ? 1 : 0][kp <= 16 ? kp : 0];
   if (c == 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return 1;
-    int cc = 0;
+    int dev = 0, cc = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 2;
     cudaDeviceGetAttribute(&cc, cudaDevAttrComputeCapabilityMajor, dev);
-    if (cc < 10) return 1;  // planning without an sm_100 device (workspace sizing)
-    c = dtype == ATKG_BF16 ? stream_occupancy<__nv_bfloat16>(kp) : stream_occupancy<float>(kp);
+    if (cc < 10) return 2;  // planning without an sm_100 device (workspace sizing)
+    c = dtype == ATKG_BF16 ? flat_occupancy<__nv_bfloat16>(kp) : flat_occupancy<float>(kp);
   }
   return c;
 }
 
+struct S1Plan {
+  enum Kind { kGeneric, kFlat, kSegments } kind = kGeneric;
+  int V = 4;
+  uint64_t nstr = 0;
+  uint32_t tiles = 0;
+  // flat
+  uint64_t units = 0, total = 0, len = 0, warps = 0;
+  uint32_t parts = 1;
+  // segments
+  uint32_t segs = 0, cpr = 0, group = 1;
+  uint64_t groups = 0, seg_len = 0;
+  size_t smem = 0;
+};
+
+// rows x (nstr stride-rows of B buckets), row_stride elements apart
+S1Plan plan_stage1(int dtype, const void* in, uint64_t rows, uint64_t len, uint64_t row_stride, uint64_t B,
+                   uint32_t kp) {
+  S1Plan pl;
+  const int esz = dtype == ATKG_BF16 ? 2 : 4;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(in);
+  pl.nstr = len / B;
+  if (!kp_specialised(kp) || pl.nstr == 0) return pl;
+  const int Vf = flat_vec(kp, esz);
+  const bool tma_ok = (addr % 16 == 0) && ((row_stride * esz) % 16 == 0) && ((B * esz) % 16 == 0) && (B % Vf == 0);
+  if (tma_ok && env_u64("ATKG_NO_FLAT", 0) == 0) {
+    pl.kind = S1Plan::kFlat;
+    pl.V = Vf;
+    pl.tiles = static_cast<uint32_t>(ceil_div(B, 32ull * Vf));
+    pl.units = rows * pl.tiles;
+    pl.total = pl.units * pl.nstr;
+    const uint64_t target = env_u64("ATKG_WARPS", static_cast<uint64_t>(sm_count()) * flat_ctas_per_sm(dtype, kp) * kFlatWarps);
+    pl.len = std::max<uint64_t>(1, ceil_div(pl.total, std::max<uint64_t>(1, target)));
+    pl.warps = ceil_div(pl.total, pl.len);
+    pl.parts = static_cast<uint32_t>(ceil_div(pl.nstr, pl.len) + 1);
+    return pl;
+  }
+  const bool aligned = (addr % (4 * esz) == 0) && (row_stride % 4 == 0) && (B % 4 == 0);
+  if (!aligned) return pl;
+  pl.kind = S1Plan::kSegments;
+  pl.V = 4;
+  pl.tiles = static_cast<uint32_t>(ceil_div(B, 128ull));
+  const uint64_t units = rows * pl.tiles;
+  const uint64_t target_warps = static_cast<uint64_t>(sm_count()) * 32;
+  const uint64_t min_len = std::max<uint64_t>(kp, 32);
+  const uint64_t max_segs = std::max<uint64_t>(1, pl.nstr / min_len);
+  const uint64_t segs = std::min<uint64_t>(max_segs, std::max<uint64_t>(1, ceil_div(target_warps, units)));
+  pl.seg_len = std::max<uint64_t>(1, ceil_div(pl.nstr, segs));
+  if (pl.nstr >= kp) pl.seg_len = std::max<uint64_t>(pl.seg_len, kp);
+  pl.segs = static_cast<uint32_t>(std::max<uint64_t>(1, ceil_div(pl.nstr, pl.seg_len)));
+  pl.group = 1;
+  while (pl.group < (uint32_t)kSegWarps && pl.group < pl.segs) pl.group <<= 1;
+  pl.cpr = static_cast<uint32_t>(ceil_div(pl.segs, pl.group));
+  pl.parts = pl.cpr;
+  pl.groups = rows * pl.tiles * pl.cpr;
+  pl.smem = pl.group > 1 ? static_cast<size_t>(kSegWarps / 2) * (2 * kp + 2) * 4 * 32 * 4 : 0;
+  return pl;
+}
+
+uint64_t stage1_ws_bytes(const S1Plan& pl, uint64_t rows, uint64_t B, uint32_t kp) {
+  if (pl.kind == S1Plan::kGeneric) return 0;
+  return align_up(rows * pl.parts * (2ull * kp + 2) * B * 4);
+}
+
 template <typename T, int KP>
-void launch_segments(const S1Plan& pl, const SegArgs& a, cudaStream_t st) {
-  const uint64_t grid = ceil_div(pl.groups, pl.warps / pl.group);
-  if (pl.stream) {
-    auto kern = stage1_stream_kernel<T, KP, stream_vec(KP), kStreamWarps, kStreamSlots, kStreamRows, kLogCap, stream_q0(KP)>;
-    constexpr size_t smem = stream_smem<T, KP>();
+void launch_stage1(const S1Plan& pl, const void* in, uint64_t rows, uint64_t row_stride, uint64_t B,
+                   uint64_t index_offset, uint32_t* out, uint32_t* status, cudaStream_t st) {
+  if (pl.kind == S1Plan::kFlat) {
+    FlatArgs a{};
+    a.in = in;
+    a.row_stride = row_stride;
+    a.B = B;
+    a.nstr = pl.nstr;
+    a.index_offset = index_offset;
+    a.total = pl.total;
+    a.len = pl.len;
+    a.tiles = pl.tiles;
+    a.parts = pl.parts;
+    a.warps = pl.warps;
+    a.out = out;
+    a.status = status;
+    auto kern = flat_kernel_fn<T, KP>();
+    constexpr size_t smem = flat_smem<T, KP>();
     static bool attr = false;
     if (!attr) {
       CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr = true;
     }
     g_prof.bracket_begin(st);
-    kern<<<static_cast<unsigned>(grid), kStreamWarps * 32, smem, st>>>(a);
+    kern<<<static_cast<unsigned>(ceil_div(pl.warps, kFlatWarps)), kFlatWarps * 32, smem, st>>>(a);
     check_launch();
     g_prof.bracket_end(st);
     return;
   }
+  SegArgs a{};
+  a.in = in;
+  a.row_stride = row_stride;
+  a.rows = rows;
+  a.B = B;
+  a.nstr = pl.nstr;
+  a.index_offset = index_offset;
+  a.seg_len = pl.seg_len;
+  a.segs = pl.segs;
+  a.cta_per_row_tile = pl.cpr;
+  a.group = pl.group;
+  a.groups = pl.groups;
+  a.tiles = pl.tiles;
+  a.out = out;
+  a.status = status;
   auto kern = stage1_segments_kernel<T, KP, 4, kSegWarps, kPrefetch>;
   static bool attr = false;
   if (!attr) {
@@ -236,24 +290,34 @@ void launch_segments(const S1Plan& pl, const SegArgs& a, cudaStream_t st) {
     attr = true;
   }
   g_prof.bracket_begin(st);
-  kern<<<static_cast<unsigned>(grid), kSegWarps * 32, pl.smem, st>>>(a);
+  kern<<<static_cast<unsigned>(ceil_div(pl.groups, kSegWarps / pl.group)), kSegWarps * 32, pl.smem, st>>>(a);
   check_launch();
   g_prof.bracket_end(st);
 }
 
-template <typename T>
-void dispatch_segments(uint32_t kp, const S1Plan& pl, const SegArgs& a, cudaStream_t st) {
-  switch (kp) {
-    case 1: launch_segments<T, 1>(pl, a, st); break;
-    case 2: launch_segments<T, 2>(pl, a, st); break;
-    case 3: launch_segments<T, 3>(pl, a, st); break;
-    case 4: launch_segments<T, 4>(pl, a, st); break;
-    case 5: launch_segments<T, 5>(pl, a, st); break;
-    case 6: launch_segments<T, 6>(pl, a, st); break;
-    case 7: launch_segments<T, 7>(pl, a, st); break;
-    case 8: launch_segments<T, 8>(pl, a, st); break;
-    case 16: launch_segments<T, 16>(pl, a, st); break;
-    default: throw Unsupported("local_k has no specialised stage-1 kernel");
+#define ATKG_KP_SWITCH(kp, CALL)                   \
+  switch (kp) {                                    \
+    case 1: { constexpr int K_ = 1; CALL; } break;  \
+    case 2: { constexpr int K_ = 2; CALL; } break;  \
+    case 3: { constexpr int K_ = 3; CALL; } break;  \
+    case 4: { constexpr int K_ = 4; CALL; } break;  \
+    case 5: { constexpr int K_ = 5; CALL; } break;  \
+    case 6: { constexpr int K_ = 6; CALL; } break;  \
+    case 7: { constexpr int K_ = 7; CALL; } break;  \
+    case 8: { constexpr int K_ = 8; CALL; } break;  \
+    case 16: { constexpr int K_ = 16; CALL; } break; \
+    default: throw Unsupported("local_k has no specialised kernel"); \
+  }
+
+// stage-1 summaries of rows x (len elements) into ws (plan kinds flat/segments)
+void run_stage1_summaries(int dtype, const S1Plan& pl, const void* in, uint64_t rows, uint64_t row_stride,
+                          uint64_t B, uint32_t kp, uint64_t index_offset, void* ws, uint32_t* status,
+                          cudaStream_t st) {
+  uint32_t* out = static_cast<uint32_t*>(ws);
+  if (dtype == ATKG_BF16) {
+    ATKG_KP_SWITCH(kp, (launch_stage1<__nv_bfloat16, K_>(pl, in, rows, row_stride, B, index_offset, out, status, st)));
+  } else {
+    ATKG_KP_SWITCH(kp, (launch_stage1<float, K_>(pl, in, rows, row_stride, B, index_offset, out, status, st)));
   }
 }
 
@@ -269,23 +333,33 @@ void launch_merge(const uint32_t* in, uint32_t parts, uint64_t rows, uint64_t B,
 void dispatch_merge(uint32_t kp, const uint32_t* in, uint32_t parts, uint64_t rows, uint64_t B, float* gv,
                     uint32_t* gi, uint64_t gstride, uint32_t* summ_out, cudaStream_t st,
                     const uint32_t* prefix = nullptr) {
-  switch (kp) {
-    case 1: launch_merge<1>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
-    case 2: launch_merge<2>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
-    case 3: launch_merge<3>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
-    case 4: launch_merge<4>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
-    case 5: launch_merge<5>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
-    case 6: launch_merge<6>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
-    case 7: launch_merge<7>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
-    case 8: launch_merge<8>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
-    case 16: launch_merge<16>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st); break;
-    default: throw Unsupported("local_k has no specialised merge kernel");
-  }
+  ATKG_KP_SWITCH(kp, (launch_merge<K_>(in, parts, rows, B, gv, gi, gstride, summ_out, prefix, st)));
 }
 
-uint64_t stage1_ws_bytes(const S1Plan& pl, uint64_t rows, uint64_t B, uint32_t kp) {
-  if (pl.generic) return 0;
-  return align_up(rows * pl.cpr * (2ull * kp + 2) * B * 4);
+template <int KP>
+void launch_merge_parts(const S1Plan& pl, const uint32_t* in, uint64_t rows, uint64_t B, float* gv, uint32_t* gi,
+                        uint64_t gstride, uint32_t* summ_out, cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>(rows * ceil_div(B, 32));
+  if (pl.parts >= 32)
+    merge_parts_kernel<KP, 8><<<grid, 256, 0, st>>>(in, pl.parts, pl.nstr, pl.len, pl.tiles, pl.V, rows, B, gv, gi,
+                                                     gstride, summ_out);
+  else if (pl.parts >= 8)
+    merge_parts_kernel<KP, 4><<<grid, 128, 0, st>>>(in, pl.parts, pl.nstr, pl.len, pl.tiles, pl.V, rows, B, gv, gi,
+                                                     gstride, summ_out);
+  else
+    merge_parts_kernel<KP, 1><<<grid, 32, 0, st>>>(in, pl.parts, pl.nstr, pl.len, pl.tiles, pl.V, rows, B, gv, gi,
+                                                    gstride, summ_out);
+  check_launch();
+}
+
+// folds the summaries of run_stage1_summaries: grid (Alg. 1 state) and/or merged summary
+void run_merge(const S1Plan& pl, uint32_t kp, const uint32_t* ws, uint64_t rows, uint64_t B, float* gv,
+               uint32_t* gi, uint64_t gstride, uint32_t* summ_out, cudaStream_t st) {
+  if (pl.kind == S1Plan::kFlat) {
+    ATKG_KP_SWITCH(kp, (launch_merge_parts<K_>(pl, ws, rows, B, gv, gi, gstride, summ_out, st)));
+  } else {
+    dispatch_merge(kp, ws, pl.parts, rows, B, gv, gi, gstride, summ_out, st);
+  }
 }
 
 // stage 1 into a grid (grid_stride elements between rows)
@@ -294,7 +368,7 @@ void run_stage1_grid(int dtype, const void* in, uint64_t rows, const atkg_params
   const uint64_t B = p.num_buckets;
   const uint32_t kp = p.local_k;
   const S1Plan pl = plan_stage1(dtype, in, rows, p.n, p.n, B, kp);
-  if (pl.generic) {
+  if (pl.kind == S1Plan::kGeneric) {
     if (gstride != kp * B) throw Unsupported("generic stage 1 needs a dense grid");
     const uint64_t threads = rows * B;
     if (dtype == ATKG_BF16)
@@ -306,24 +380,8 @@ void run_stage1_grid(int dtype, const void* in, uint64_t rows, const atkg_params
     check_launch();
     return;
   }
-  SegArgs a{};
-  a.in = in;
-  a.row_stride = p.n;
-  a.rows = rows;
-  a.B = B;
-  a.nstr = pl.nstr;
-  a.index_offset = 0;
-  a.seg_len = pl.seg_len;
-  a.segs = pl.segs;
-  a.cta_per_row_tile = pl.cpr;
-  a.group = pl.group;
-  a.groups = pl.groups;
-  a.tiles = pl.tiles;
-  a.out = static_cast<uint32_t*>(ws);
-  a.status = status;
-  if (dtype == ATKG_BF16) dispatch_segments<__nv_bfloat16>(kp, pl, a, st);
-  else dispatch_segments<float>(kp, pl, a, st);
-  dispatch_merge(kp, a.out, pl.cpr, rows, B, gv, gi, gstride, nullptr, st);
+  run_stage1_summaries(dtype, pl, in, rows, p.n, B, kp, 0, ws, status, st);
+  run_merge(pl, kp, static_cast<const uint32_t*>(ws), rows, B, gv, gi, gstride, nullptr, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -396,6 +454,37 @@ uint64_t grid_bytes(uint64_t rows, const atkg_params& p) { return align_up(rows 
 
 uint64_t filled_count(const atkg_params& p) {  // topk.cpp:250-253
   return std::min<uint64_t>(p.local_k, p.n / p.num_buckets) * p.num_buckets;
+}
+
+// fused merge + stage 2 (merge_select_kernel) for the flat path
+size_t merge_select_smem(const S1Plan& pl, const atkg_params& p) {
+  const uint64_t words = (2ull * p.local_k + 2) * p.num_buckets;
+  const uint64_t staged = (pl.parts * words + 3) & ~3ull;
+  return staged * 4 + (size_t)next_pow2(filled_count(p)) * 8;
+}
+bool fused_tail_ok(const S1Plan& pl, const atkg_params& p) {
+  return pl.kind == S1Plan::kFlat && merge_select_smem(pl, p) <= 200 * 1024 &&
+         next_pow2(filled_count(p)) <= kMaxSortKeys && ((2ull * p.local_k + 2) * p.num_buckets) % 4 == 0;
+}
+template <int KP>
+void launch_merge_select(const S1Plan& pl, const atkg_params& p, const uint32_t* ws, uint64_t rows, float* ov,
+                         uint32_t* oi, float* gv, uint32_t* gi, uint32_t* status, cudaStream_t st) {
+  const size_t smem = merge_select_smem(pl, p);
+  static size_t attr = 0;
+  if (attr < smem) {
+    CUDA_OK(cudaFuncSetAttribute(merge_select_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const uint32_t P = next_pow2(filled_count(p));
+  const uint32_t threads = std::min<uint32_t>(512, std::max<uint32_t>(64, (uint32_t)std::max<uint64_t>(p.num_buckets, P / 2)));
+  const uint32_t filled = (uint32_t)std::min<uint64_t>(p.local_k, p.n / p.num_buckets);
+  merge_select_kernel<KP><<<static_cast<unsigned>(rows), (threads + 31) / 32 * 32, smem, st>>>(
+      ws, pl.parts, pl.nstr, pl.len, pl.tiles, pl.V, p.num_buckets, filled, P, p.global_k, ov, oi, gv, gi, status);
+  check_launch();
+}
+void run_merge_select(const S1Plan& pl, const atkg_params& p, const uint32_t* ws, uint64_t rows, float* ov,
+                      uint32_t* oi, float* gv, uint32_t* gi, uint32_t* status, cudaStream_t st) {
+  ATKG_KP_SWITCH(p.local_k, (launch_merge_select<K_>(pl, p, ws, rows, ov, oi, gv, gi, status, st)));
 }
 
 // ---------------------------------------------------------------------------
@@ -550,6 +639,13 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     float* gv = reinterpret_cast<float*>(w);
     uint32_t* gi = reinterpret_cast<uint32_t*>(w + rows * gstride * 4);
     w += grid_bytes(rows, *p);
+    if (fused_tail_ok(pl, *p)) {
+      // stage 1 summaries, then one fused merge + stage-2 kernel per row
+      run_stage1_summaries(dtype, pl, d_in, rows, p->n, p->num_buckets, p->local_k, 0, s1ws, d_status, st);
+      run_merge_select(pl, *p, static_cast<const uint32_t*>(s1ws), rows, d_out_vals, d_out_idx, nullptr, nullptr,
+                       d_status, st);
+      return;
+    }
     run_stage1_grid(dtype, d_in, rows, *p, gv, gi, gstride, s1ws, d_status, st);
     run_select(gv, gi, rows, filled_count(*p), gstride, p->global_k, UINT64_MAX, d_out_vals, d_out_idx, w,
                d_status, st);
@@ -587,26 +683,10 @@ int atkg_stage1_summary(int dtype, const void* d_slice, uint64_t len, uint64_t i
     if (!kp_specialised(p->local_k)) throw Unsupported("local_k has no specialised summary kernel");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const S1Plan pl = plan_stage1(dtype, d_slice, 1, len, len, B, p->local_k);
-    if (pl.generic) throw Unsupported("summary path needs num_buckets % 4 == 0 and aligned input");
+    if (pl.kind == S1Plan::kGeneric) throw Unsupported("summary path needs num_buckets % 4 == 0 and aligned input");
     char* w = reinterpret_cast<char*>(align_up(reinterpret_cast<uintptr_t>(d_ws)));
-    SegArgs a{};
-    a.in = d_slice;
-    a.row_stride = len;
-    a.rows = 1;
-    a.B = B;
-    a.nstr = pl.nstr;
-    a.index_offset = index_offset;
-    a.seg_len = pl.seg_len;
-    a.segs = pl.segs;
-    a.cta_per_row_tile = pl.cpr;
-    a.group = pl.group;
-    a.groups = pl.groups;
-    a.tiles = pl.tiles;
-    a.out = reinterpret_cast<uint32_t*>(w);
-    a.status = d_status;
-    if (dtype == ATKG_BF16) dispatch_segments<__nv_bfloat16>(p->local_k, pl, a, st);
-    else dispatch_segments<float>(p->local_k, pl, a, st);
-    dispatch_merge(p->local_k, a.out, pl.cpr, 1, B, nullptr, nullptr, 0, d_summary, st);
+    run_stage1_summaries(dtype, pl, d_slice, 1, len, B, p->local_k, index_offset, w, d_status, st);
+    run_merge(pl, p->local_k, reinterpret_cast<const uint32_t*>(w), 1, B, nullptr, nullptr, 0, d_summary, st);
   });
 }
 
@@ -796,20 +876,6 @@ void launch_fold(uint32_t* summ, uint64_t B, const void* blk, uint64_t start, ui
       summ, B, static_cast<const T*>(blk), start, count, status);
   check_launch();
 }
-#define ATKG_KP_SWITCH(kp, CALL)                   \
-  switch (kp) {                                    \
-    case 1: { constexpr int K_ = 1; CALL; } break;  \
-    case 2: { constexpr int K_ = 2; CALL; } break;  \
-    case 3: { constexpr int K_ = 3; CALL; } break;  \
-    case 4: { constexpr int K_ = 4; CALL; } break;  \
-    case 5: { constexpr int K_ = 5; CALL; } break;  \
-    case 6: { constexpr int K_ = 6; CALL; } break;  \
-    case 7: { constexpr int K_ = 7; CALL; } break;  \
-    case 8: { constexpr int K_ = 8; CALL; } break;  \
-    case 16: { constexpr int K_ = 16; CALL; } break; \
-    default: throw Unsupported("local_k has no specialised kernel"); \
-  }
-
 void acc_fold(atkg_accumulator* a, int dtype, const void* blk, uint64_t start, uint64_t count, cudaStream_t st) {
   if (count == 0) return;
   const uint64_t B = a->p.num_buckets;
@@ -872,31 +938,20 @@ int atkg_accumulator_consume(atkg_accumulator* a, int dtype, const void* d_block
       const uint64_t body = (end - h) / B * B;
       const void* bptr = blk + (h - start) * esz;
       const S1Plan pl = plan_stage1(dtype, bptr, 1, body, body, B, a->p.local_k);
-      if (body > 0 && !pl.generic) {
-        const size_t need = stage1_ws_bytes(pl, 1, B, a->p.local_k);
+      if (body > 0 && pl.kind != S1Plan::kGeneric) {
+        const size_t words = (2ull * a->p.local_k + 2) * B * 4;
+        const size_t need = stage1_ws_bytes(pl, 1, B, a->p.local_k) + align_up(words);
         if (a->ws_cap < need) {
           if (a->ws) CUDA_OK(cudaFree(a->ws));
           CUDA_OK(cudaMalloc(&a->ws, need));
           a->ws_cap = need;
         }
-        SegArgs s{};
-        s.in = bptr;
-        s.row_stride = body;
-        s.rows = 1;
-        s.B = B;
-        s.nstr = pl.nstr;
-        s.index_offset = h;
-        s.seg_len = pl.seg_len;
-        s.segs = pl.segs;
-        s.cta_per_row_tile = pl.cpr;
-        s.group = pl.group;
-        s.groups = pl.groups;
-        s.tiles = pl.tiles;
-        s.out = static_cast<uint32_t*>(a->ws);
-        s.status = a->status;
-        if (dtype == ATKG_BF16) dispatch_segments<__nv_bfloat16>(a->p.local_k, pl, s, st);
-        else dispatch_segments<float>(a->p.local_k, pl, s, st);
-        dispatch_merge(a->p.local_k, s.out, pl.cpr, 1, B, nullptr, nullptr, 0, a->summ, st, a->summ);
+        uint32_t* parts = static_cast<uint32_t*>(a->ws);
+        uint32_t* body_summ = reinterpret_cast<uint32_t*>(static_cast<char*>(a->ws) + stage1_ws_bytes(pl, 1, B, a->p.local_k));
+        run_stage1_summaries(dtype, pl, bptr, 1, body, B, a->p.local_k, h, parts, a->status, st);
+        run_merge(pl, a->p.local_k, parts, 1, B, nullptr, nullptr, 0, body_summ, st);
+        // acc = merge(acc, body) in index order
+        dispatch_merge(a->p.local_k, body_summ, 1, 1, B, nullptr, nullptr, 0, a->summ, st, a->summ);
         acc_fold(a, dtype, blk + (h + body - start) * esz, h + body, end - h - body, st);
       } else {
         acc_fold(a, dtype, blk + (h - start) * esz, h, end - h, st);

@@ -27,6 +27,7 @@
 
 #include "common.cuh"
 #include "ptx.cuh"
+#include "stage2.cuh"
 
 namespace atkg {
 
@@ -536,6 +537,7 @@ __device__ __forceinline__ void lds_vec(const uint8_t* p, float (&out)[V]) {
   VecLoad<T, V>::unpack(w, out);
 }
 
+// ---------------------------------------------------------------------------
 // Hot loop = filter -> log -> flush.  Per element the common path is one
 // compare against a per-bucket threshold f plus a predicated append to a
 // per-lane log in shared memory -- 4 instructions, no branch, full SIMT
@@ -544,243 +546,417 @@ __device__ __forceinline__ void lds_vec(const uint8_t* p, float (&out)[V]) {
 // algorithm would send down its slow path (plus some it rejects on replay).
 // A flush replays each lane's logs in index order through the exact summary
 // update (Summ::push), warp-synchronously, then raises f.
-// Loads are 128-bit (V elements per lane), D stride-rows per block with the
-// next block prefetched into registers while the current one is filtered.
 // Log layout per warp (structure of arrays, lane-minor, conflict-free):
 //   float    val[V][LOGC][32]   element value
-//   uint16_t row[V][LOGC][32]   stride-row offset j - j0 of the element
-__device__ __forceinline__ void log_append(uint32_t& pv, uint32_t& pj, float x, float f, uint16_t jrel) {
-  // appends (x, jrel) when !(x < f) -- NaN included -- and bumps both cursors
+//   uint32_t row[V][LOGC][32]   stride-row index j of the element
+// ---------------------------------------------------------------------------
+template <int ROWOFF>
+__device__ __forceinline__ void log_append(uint32_t& pv, float x, float f, uint32_t j) {
+  // appends (x, j) when !(x < f) -- NaN included -- and bumps the cursor;
+  // the row array sits ROWOFF bytes after the value array
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "setp.geu.f32 p, %2, %3;\n\t"
-      "@p st.shared.f32 [%0], %2;\n\t"
-      "@p st.shared.u16 [%1], %4;\n\t"
-      "@p add.u32 %0, %0, 128;\n\t"
-      "@p add.u32 %1, %1, 64;\n\t}"
-      : "+r"(pv), "+r"(pj)
-      : "f"(x), "f"(f), "h"(jrel)
+      "setp.geu.f32 p, %1, %2;\n\t"
+      "@p st.shared.f32 [%0], %1;\n\t"
+      "@p st.shared.u32 [%0+%4], %3;\n\t"
+      "@p add.u32 %0, %0, 128;\n\t}"
+      : "+r"(pv)
+      : "f"(x), "f"(f), "r"(j), "n"(ROWOFF)
       : "memory");
 }
 
+// Balanced flat partition.  The work is the flattened space of
+// (unit = (row, 32V-bucket tile), stride-row j) pairs, cut into equal
+// contiguous ranges, one per warp, so every SM streams the same number of
+// bytes whatever the row count.  A warp walks its range in chunks of CR
+// stride-rows (never crossing a unit), fed by its own ring of NS shared-memory
+// slots that 1-D TMA bulk copies (cp.async.bulk -> UBLKCP) keep full.  Each
+// unit piece of the range yields one exact summary, stored as part
+// (w - first warp of the unit) of that unit; merge_parts_kernel folds a unit's
+// parts in index order.
+//
+// Before filtering a piece, the warp takes tau = K'-th largest value of the
+// piece's first Q0 stride-rows (a value-only sorting network).  Any subset's
+// K'-th value is a lower bound of the bucket's final K'-th value v*, and
+// Alg. 1 over any subsequence that contains every element >= v* ends in the
+// same state, so filtering with f >= tau from the first element on is exact
+// -- and skips the cold start of every piece.
+struct FlatArgs {
+  const void* in;
+  uint64_t row_stride;    // elements between rows
+  uint64_t B;             // buckets
+  uint64_t nstr;          // stride-rows per unit
+  uint64_t index_offset;  // position of the first element (slice sharding)
+  uint64_t total;         // units * nstr
+  uint64_t len;           // stride-rows per warp
+  uint32_t tiles;         // ceil(B / 32V)
+  uint32_t parts;         // part slots per unit
+  uint64_t warps;         // warps in the grid with work
+  uint32_t* out;          // summary blocks [rows][parts][words(B)]
+  uint32_t* status;
+};
+
 template <typename T, int KP, int V, int W, int NS, int CR, int LOGC, int Q0>
 __global__ void __launch_bounds__(W * 32)
-stage1_stream_kernel(SegArgs a) {
+stage1_flat_kernel(FlatArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  static_assert(LOGC >= 2 * CR, "log must absorb a chunk between flush checks");
+  static_assert(LOGC > CR, "log must absorb a chunk between flush checks");
   constexpr int LB = V * sizeof(T);              // bytes per lane per stride-row
   constexpr int SB = CR * 32 * LB;               // bytes per ring slot
   constexpr int RING = NS * SB;
   constexpr int LOGV = V * LOGC * 32;            // log entries per warp
-  constexpr int WARP_BYTES = RING + LOGV * 6;    // ring + val[] + row[]
+  constexpr int WARP_BYTES = RING + LOGV * 8;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   uint8_t* ring = smem_raw + warp * WARP_BYTES;
   uint8_t* lbase = ring + RING;
   const float* logv = reinterpret_cast<const float*>(lbase);
-  const uint16_t* logj = reinterpret_cast<const uint16_t*>(lbase + LOGV * 4);
+  const uint32_t* logj = reinterpret_cast<const uint32_t*>(lbase + LOGV * 4);
   const uint32_t sv0 = (uint32_t)__cvta_generic_to_shared(lbase) + lane * 4;
-  const uint32_t sj0 = (uint32_t)__cvta_generic_to_shared(lbase + LOGV * 4) + lane * 2;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + W * WARP_BYTES) + warp * NS;
-
-  const uint32_t G = a.group;
-  const int gw = warp & (G - 1);
-  uint64_t grp = (uint64_t)blockIdx.x * (W / G) + warp / G;
-  const bool grp_ok = grp < a.groups;
-  const uint32_t cseg = (uint32_t)(grp % a.cta_per_row_tile);
-  grp /= a.cta_per_row_tile;
-  const uint32_t tile = (uint32_t)(grp % a.tiles);
-  const uint64_t row = grp / a.tiles;
-  const uint64_t tb0 = (uint64_t)tile * 32 * V;
-  const uint64_t b0 = tb0 + (uint64_t)lane * V;
-  const bool lane_ok = grp_ok && b0 < a.B;
-  const uint32_t seg = cseg * G + gw;
+  const uint64_t w = (uint64_t)blockIdx.x * W + warp;
+  if (w >= a.warps) return;  // warp-uniform; no CTA-wide barriers below
+  const uint64_t F0 = w * a.len;
+  const uint64_t F1 = umin64(F0 + a.len, a.total);
   const uint64_t B = a.B;
-  const uint64_t j0 = (uint64_t)seg * a.seg_len;
-  // trip counts are warp-uniform (warp-synchronous flushes); lanes past the
-  // last bucket read lane 0's data (real input, so a NaN there is a real
-  // NaN) and filter with f = +inf
-  const uint64_t j1 = (grp_ok && seg < a.segs) ? umin64(j0 + a.seg_len, a.nstr) : j0;
-  const uint32_t ioff = (uint32_t)(a.index_offset + b0);
-  const uint32_t Bu = (uint32_t)B;
-  const uint32_t tw = grp_ok ? (uint32_t)(umin64(32 * V, B - tb0) * sizeof(T)) : 0u;  // bytes per row
-  const bool contiguous = (a.tiles == 1) && ((uint64_t)tw == B * sizeof(T));
-  const uint32_t nch = (uint32_t)((j1 - j0 + CR - 1) / CR);
-  const char* gbase = reinterpret_cast<const char*>(a.in) + (row * a.row_stride + tb0) * sizeof(T);
   const uint64_t gstride = B * sizeof(T);
-  const uint32_t lane_off = lane_ok ? lane * LB : 0u;
+  const uint32_t Bu = (uint32_t)B;
 
-  // ---- TMA ring: lane 0 keeps NS chunks of CR stride-rows in flight --------
-  if (lane == 0) {
-#pragma unroll
-    for (int q = 0; q < NS; ++q) ptx::mbar_init(&bars[q], 1);
-    ptx::fence_mbar_init();
-  }
-  __syncwarp();
-  const uint64_t pol = ptx::policy_evict_first();
-  auto issue = [&](uint32_t c) {
-    const uint32_t slot = c % NS;
-    const uint64_t jr = j0 + (uint64_t)c * CR;
-    const uint32_t rows = (uint32_t)umin64(CR, j1 - jr);
-    ptx::mbar_arrive_expect_tx(&bars[slot], rows * tw);
-    if (contiguous) {
-      ptx::bulk_g2s(ring + slot * SB, gbase + jr * gstride, rows * tw, &bars[slot], pol);
-    } else {
-      for (uint32_t r = 0; r < rows; ++r)
-        ptx::bulk_g2s(ring + slot * SB + r * tw, gbase + (jr + r) * gstride, tw, &bars[slot], pol);
-    }
+  // chunk sequence of this warp: [F, F + rows) with rows <= CR, cut at unit
+  // ends; producer and consumer walk it incrementally (no divisions per chunk)
+  auto unit_src = [&](uint64_t u, uint32_t& tw, bool& contiguous) -> const char* {
+    const uint64_t row = u / a.tiles, tile = u - row * a.tiles;
+    const uint64_t tb0 = tile * 32 * V;
+    tw = (uint32_t)(umin64(32 * V, B - tb0) * sizeof(T));
+    contiguous = (a.tiles == 1) && ((uint64_t)tw == gstride);
+    return reinterpret_cast<const char*>(a.in) + (row * a.row_stride + tb0) * sizeof(T);
   };
-  if (lane == 0)
-    for (uint32_t c = 0; c < (nch < (uint32_t)NS ? nch : (uint32_t)NS); ++c) issue(c);
 
-  Summ<KP> s[V];
-  float f[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) { s[v].clear(); f[v] = neg_inf(); }
-  uint32_t nan = 0;
-
-  // ---- phase 0: threshold from a sample ------------------------------------
-  // Each warp takes the top-KP values (a sorting network on values only) of
-  // the first Q0 stride-rows of its segment; the warps of a group (same row
-  // and tile) pool them in shared memory and every bucket gets
-  // tau = KP-th largest of the pooled sample.  Any subset's KP-th value is a
-  // lower bound of the bucket's final KP-th value v*, and Alg. 1 over any
-  // subsequence that contains every element >= v* ends in the same state, so
-  // filtering with f >= tau from the first element on is exact -- and skips
-  // the cold start of every segment.  (The sample reads go through L2, where
-  // the ring's bulk copies of the same rows then hit.)
-  {
-    float net[V][KP];
-#pragma unroll
-    for (int v = 0; v < V; ++v)
-#pragma unroll
-      for (int k = 0; k < KP; ++k) net[v][k] = neg_inf();
-    const T* sbase = reinterpret_cast<const T*>(gbase + lane_off);
-    const uint64_t qend = umin64(j0 + Q0, j1);
-    for (uint64_t q = j0; q < qend; ++q) {
-      float x[V];
-      VecLoad<T, V>::load(sbase + q * B, x);
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        float c = x[v];
-        if (c != c) c = neg_inf();  // NaN is caught by the filter below
-#pragma unroll
-        for (int k = 0; k < KP; ++k) {
-          const float hi = fmaxf(net[v][k], c);
-          c = fminf(net[v][k], c);
-          net[v][k] = hi;
-        }
+  // ---- ring fill: every lane copies its own LB bytes of each stride-row ----
+  // (cp.async -> LDGSTS; a lane only ever reads back what it copied, so the
+  // per-thread wait_group is the only synchronisation the ring needs)
+  uint64_t Fi = F0;
+  uint64_t ui = F0 / a.nstr;
+  uint64_t ji = F0 - ui * a.nstr;
+  uint32_t ci = 0, twi = 0;
+  bool conti = false;
+  const char* srci = unit_src(ui, twi, conti);
+  uint32_t lofi = ((uint64_t)lane * LB < twi) ? lane * LB : 0u;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  auto issue_next = [&]() {  // all lanes; always commits one group
+    if (Fi < F1) {
+      if (ji == a.nstr) {
+        ++ui;
+        ji = 0;
+        srci = unit_src(ui, twi, conti);
+        lofi = ((uint64_t)lane * LB < twi) ? lane * LB : 0u;
       }
+      const uint32_t slot = ci % NS;
+      const uint64_t left = umin64(F1 - Fi, a.nstr - ji);
+      const uint32_t dst = ring_s + slot * SB;
+      if (conti && twi == 32 * LB && left >= CR) {
+        // full tile, full chunk: one contiguous CR x 32LB block, lanes stride
+        // through it with compile-time offsets
+        const char* src = srci + ji * gstride + lane * LB;
+#pragma unroll
+        for (int r = 0; r < CR; ++r) ptx::cp_async<LB>(dst + r * 32 * LB + lane * LB, src + r * 32 * LB);
+        Fi += CR;
+        ji += CR;
+      } else {
+        const uint32_t rows = (uint32_t)umin64(CR, left);
+        const char* src = srci + ji * gstride + lofi;
+        for (uint32_t r = 0; r < rows; ++r) {
+          ptx::cp_async<LB>(dst + r * twi + lofi, src);
+          src += gstride;
+        }
+        Fi += rows;
+        ji += rows;
+      }
+      ++ci;
     }
-    // exchange area: the (still unused) log of every warp
-    float* mine = reinterpret_cast<float*>(lbase);
+    ptx::cp_async_commit();
+  };
 #pragma unroll
-    for (int k = 0; k < KP; ++k)
+  for (int q = 0; q < NS - 1; ++q) issue_next();
+
+  uint32_t nan = 0;
+  uint64_t F = F0;  // consumer position
+  uint32_t c = 0;   // chunks consumed
+  while (F < F1) {
+    // ---- a unit piece: [F, piece_end) of unit u ----------------------------
+    const uint64_t u = F / a.nstr;  // once per piece
+    const uint64_t piece_end = umin64((u + 1) * a.nstr, F1);
+    const uint64_t row = u / a.tiles, tile = u - row * a.tiles;
+    const uint64_t b0 = (tile * 32 + lane) * V;
+    const bool lane_ok = b0 < B;
+    const uint32_t ioff = (uint32_t)(a.index_offset + b0);
+    const uint64_t jp0 = F - u * a.nstr;
+    const uint64_t plen = piece_end - F;
+    const uint32_t lane_off = lane_ok ? lane * LB : 0u;
+
+    Summ<KP> s[V];
+    float f[V], tau[V];
+    {
+      // threshold tau from the piece's first Q0 stride-rows (through L2)
+      float net[V][KP];
 #pragma unroll
-      for (int v = 0; v < V; ++v) mine[(k * V + v) * 32 + lane] = net[v][k];
-    __syncthreads();
-    const int g0 = warp - gw;
-    for (int w2 = g0; w2 < g0 + (int)G; ++w2) {
-      if (w2 == warp) continue;
-      const float* other = reinterpret_cast<const float*>(smem_raw + w2 * WARP_BYTES + RING);
+      for (int v = 0; v < V; ++v)
 #pragma unroll
-      for (int k = 0; k < KP; ++k) {
+        for (int k = 0; k < KP; ++k) net[v][k] = neg_inf();
+      const T* sbase = reinterpret_cast<const T*>(reinterpret_cast<const char*>(a.in) +
+                                                  (row * a.row_stride + tile * 32 * V) * sizeof(T) + lane_off) +
+                       jp0 * B;
+      const uint64_t qn = umin64(Q0, plen);
+      constexpr int QB = 8;
+      for (uint64_t q0 = 0; q0 < qn; q0 += QB) {
+        float x[QB][V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          float c = other[(k * V + v) * 32 + lane];
+        for (int r = 0; r < QB; ++r) {
+          if (q0 + r < qn) VecLoad<T, V>::load(sbase + (q0 + r) * B, x[r]);
+          else {
 #pragma unroll
-          for (int kk = 0; kk < KP; ++kk) {
-            const float hi = fmaxf(net[v][kk], c);
-            c = fminf(net[v][kk], c);
-            net[v][kk] = hi;
+            for (int v = 0; v < V; ++v) x[r][v] = neg_inf();
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < QB; ++r) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            float cc = x[r][v];
+            if (cc != cc) cc = neg_inf();  // NaN is caught by the filter below
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+              const float hi = fmaxf(net[v][k], cc);
+              cc = fminf(net[v][k], cc);
+              net[v][k] = hi;
+            }
           }
         }
       }
-    }
-#pragma unroll
-    for (int v = 0; v < V; ++v) f[v] = lane_ok ? net[v][KP - 1] : __int_as_float(0x7f800000);
-    __syncthreads();  // exchange area becomes the logs
-  }
-  float tau[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) tau[v] = f[v];
-
-  uint32_t ptr[V], pj[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) { ptr[v] = sv0 + v * LOGC * 128; pj[v] = sj0 + v * LOGC * 64; }
-
-  auto flush = [&]() {
-    uint32_t cnt[V], m = 0;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      cnt[v] = (ptr[v] - (sv0 + v * LOGC * 128)) >> 7;
-      m = cnt[v] > m ? cnt[v] : m;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint32_t y = __shfl_xor_sync(0xffffffffu, m, o);
-      m = y > m ? y : m;
-    }
-    for (uint32_t e = 0; e < m; ++e) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        if (e < cnt[v]) {
-          const float x = logv[(v * LOGC + e) * 32 + lane];
-          const uint32_t jj = (uint32_t)j0 + logj[(v * LOGC + e) * 32 + lane];
-          s[v].push(x, ioff + v + jj * Bu, nan);
+        s[v].clear();
+        tau[v] = lane_ok ? net[v][KP - 1] : __int_as_float(0x7f800000);
+        f[v] = tau[v];
+      }
+    }
+    uint32_t ptr[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) ptr[v] = sv0 + v * LOGC * 128;
+    auto flush = [&]() {
+      uint32_t cnt[V], m = 0;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        cnt[v] = (ptr[v] - (sv0 + v * LOGC * 128)) >> 7;
+        m = cnt[v] > m ? cnt[v] : m;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, m, o);
+        m = y > m ? y : m;
+      }
+      for (uint32_t e = 0; e < m; ++e) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          if (e < cnt[v]) {
+            const float x = logv[(v * LOGC + e) * 32 + lane];
+            const uint32_t jj = logj[(v * LOGC + e) * 32 + lane];
+            s[v].push(x, ioff + v + jj * Bu, nan);
+          }
         }
       }
-    }
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      ptr[v] = sv0 + v * LOGC * 128;
-      pj[v] = sj0 + v * LOGC * 64;
-      f[v] = s[v].full() ? fmaxf(s[v].v[KP - 1], tau[v]) : tau[v];
-    }
-  };
+      for (int v = 0; v < V; ++v) {
+        ptr[v] = sv0 + v * LOGC * 128;
+        f[v] = s[v].full() ? fmaxf(s[v].v[KP - 1], tau[v]) : tau[v];
+      }
+    };
 
-  for (uint32_t c = 0; c < nch; ++c) {
-    const uint32_t slot = c % NS;
-    ptx::mbar_wait(&bars[slot], (c / NS) & 1u);
-    const uint32_t jrel0 = c * CR;
-    const uint32_t rows = (uint32_t)umin64(CR, j1 - (j0 + jrel0));
-    const uint8_t* sl = ring + slot * SB + lane_off;
-    if (rows == CR) {
+    uint32_t tw;
+    bool contiguous;
+    (void)unit_src(u, tw, contiguous);
+    uint32_t jabs0 = (uint32_t)jp0;
+    while (F < piece_end) {
+      const uint32_t slot = c % NS;
+      issue_next();                       // chunk c + NS - 1 into the free slot
+      ptx::cp_async_wait<NS - 1>();       // chunk c has landed (this lane's bytes)
+      const uint32_t rows = (uint32_t)umin64(CR, piece_end - F);
+      const uint8_t* sl = ring + slot * SB + lane_off;
+      if (rows == CR) {
+        // all shared-memory loads first: the appends are asm volatile with a
+        // memory clobber, so loads placed after one cannot be hoisted
+        float x[CR][V];
 #pragma unroll
-      for (int r = 0; r < CR; ++r) {
-        float x[V];
-        lds_vec<T, V>(sl + r * tw, x);
+        for (int r = 0; r < CR; ++r) lds_vec<T, V>(sl + r * tw, x[r]);
 #pragma unroll
-        for (int v = 0; v < V; ++v) log_append(ptr[v], pj[v], x[v], f[v], (uint16_t)(jrel0 + r));
+        for (int r = 0; r < CR; ++r)
+#pragma unroll
+          for (int v = 0; v < V; ++v) log_append<LOGV * 4>(ptr[v], x[r][v], f[v], jabs0 + r);
+      } else {
+        for (uint32_t r = 0; r < rows; ++r) {
+          float x[V];
+          lds_vec<T, V>(sl + r * tw, x);
+#pragma unroll
+          for (int v = 0; v < V; ++v) log_append<LOGV * 4>(ptr[v], x[v], f[v], jabs0 + r);
+        }
       }
-    } else {
-      for (uint32_t r = 0; r < rows; ++r) {
-        float x[V];
-        lds_vec<T, V>(sl + r * tw, x);
+      F += rows;
+      jabs0 += rows;
+      ++c;
+      bool need = false;
 #pragma unroll
-        for (int v = 0; v < V; ++v) log_append(ptr[v], pj[v], x[v], f[v], (uint16_t)(jrel0 + r));
-      }
+      for (int v = 0; v < V; ++v) need |= ptr[v] > sv0 + (uint32_t)(v * LOGC + (LOGC - CR - 1)) * 128;
+      if (__any_sync(0xffffffffu, need)) flush();
     }
-    __syncwarp();
-    if (lane == 0 && c + NS < nch) issue(c + NS);
-    bool need = false;
+    flush();
+    // part index of this piece within its unit
+    const uint64_t wfirst = (u * a.nstr) / a.len;
+    const uint64_t part = w - wfirst;
+    const uint64_t words = (uint64_t)(2 * KP + 2) * B;
+    uint32_t* dst = a.out + (row * a.parts + part) * words;
+    if (lane_ok) {
 #pragma unroll
-    for (int v = 0; v < V; ++v) need |= ptr[v] > sv0 + (uint32_t)(v * LOGC + (LOGC - CR - 1)) * 128;
-    if (__any_sync(0xffffffffu, need)) flush();
+      for (int v = 0; v < V; ++v)
+        if (b0 + v < B) store_summ<KP>(dst, B, b0 + v, s[v]);
+    }
   }
-  flush();
   if (nan) atomicOr(a.status, ATKG_FLAG_NAN);
-  __syncthreads();  // rings drained and logs done before the merge reuses smem
-  group_merge_store<KP, V, W>(reinterpret_cast<uint32_t*>(smem_raw), warp, lane, gw, G, lane_ok, row, cseg, b0,
-                              a, s);
 }
 
 template <typename T, int KP, int V, int W, int NS, int CR, int LOGC>
-constexpr size_t stream_smem_bytes() {
-  static_assert((size_t)KP * V * 32 * 4 <= (size_t)V * LOGC * 32 * 6, "sample must fit a warp's log area");
-  constexpr size_t work = (size_t)W * (NS * CR * 32 * V * sizeof(T) + V * LOGC * 32 * 6) + (size_t)W * NS * 8;
-  constexpr size_t merge = (size_t)(W / 2) * (2 * KP + 2) * V * 32 * 4;
-  return work > merge ? work : merge;
+constexpr size_t flat_smem_bytes() {
+  return (size_t)W * (NS * CR * 32 * V * sizeof(T) + V * LOGC * 32 * 8);
+}
+
+// ---------------------------------------------------------------------------
+// hierarchical merge of a unit's parts: CTA = 32 buckets x Y part-ranges;
+// thread (y, b) folds parts [y*n/Y, (y+1)*n/Y) of bucket b in order, then a
+// shared-memory tree folds the Y partial summaries; writes the Alg. 1 grid
+// and/or the merged summary.
+// ---------------------------------------------------------------------------
+template <int KP, int Y>
+__global__ void __launch_bounds__(32 * Y)
+merge_parts_kernel(const uint32_t* __restrict__ in, uint32_t parts, uint64_t nstr, uint64_t len, uint32_t tiles,
+                   uint32_t vec, uint64_t rows, uint64_t B, float* grid_v, uint32_t* grid_i, uint64_t grid_stride,
+                   uint32_t* summ_out) {
+  __shared__ uint32_t sm[(Y / 2 > 0 ? Y / 2 : 1) * (2 * KP + 2) * 32];
+  const int lane = threadIdx.x & 31, y = threadIdx.x >> 5;
+  const uint64_t bgroups = (B + 31) / 32;
+  const uint64_t row = blockIdx.x / bgroups;
+  const uint64_t b = (blockIdx.x % bgroups) * 32 + lane;
+  const bool ok = row < rows && b < B;
+  const uint64_t bb = ok ? b : 0;
+  // parts of this bucket's unit (row, tile)
+  const uint64_t u = row * tiles + bb / (32ull * vec);
+  const uint64_t w0 = (u * nstr) / len, w1 = ((u + 1) * nstr - 1) / len;
+  const uint32_t n = (uint32_t)(w1 - w0 + 1);
+  const uint64_t words = (uint64_t)(2 * KP + 2) * B;
+  const uint32_t* base = in + row * parts * words;
+  const uint32_t q0 = (uint32_t)((uint64_t)n * y / Y), q1 = (uint32_t)((uint64_t)n * (y + 1) / Y);
+  Summ<KP> acc;
+  acc.clear();
+  if (ok)
+    for (uint32_t q = q0; q < q1; ++q) {
+      Summ<KP> o;
+      load_summ<KP>(base + q * words, B, bb, o);
+      acc.merge_later(o);
+    }
+  // tree over y: after the step, y (y % 2step == 0) holds [y, y + 2 step)
+#pragma unroll
+  for (int step = 1; step < Y; step *= 2) {
+    uint32_t* slot = sm + (y / (2 * step)) * (2 * KP + 2) * 32;
+    if ((y % (2 * step)) == step) {
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        slot[k * 32 + lane] = __float_as_uint(acc.v[k]);
+        slot[(KP + k) * 32 + lane] = acc.p[k];
+      }
+      slot[(2 * KP) * 32 + lane] = acc.lt;
+      slot[(2 * KP + 1) * 32 + lane] = __float_as_uint(acc.ltv);
+    }
+    __syncthreads();
+    if ((y % (2 * step)) == 0 && y + step < Y) {
+      Summ<KP> o;
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        o.v[k] = __uint_as_float(slot[k * 32 + lane]);
+        o.p[k] = slot[(KP + k) * 32 + lane];
+      }
+      o.lt = slot[(2 * KP) * 32 + lane];
+      o.ltv = __uint_as_float(slot[(2 * KP + 1) * 32 + lane]);
+      acc.merge_later(o);
+    }
+    __syncthreads();
+  }
+  if (y != 0 || !ok) return;
+  if (summ_out) store_summ<KP>(summ_out + row * words, B, b, acc);
+  if (grid_v) {
+    float ov[KP];
+    uint32_t oi[KP];
+    acc.finalize(ov, oi);
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      grid_v[row * grid_stride + (uint64_t)k * B + b] = ov[k];
+      grid_i[row * grid_stride + (uint64_t)k * B + b] = oi[k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fused tail for the flat path: one CTA per row stages the row's part
+// summaries in shared memory (coalesced 16-byte loads, all in flight), every
+// thread folds its buckets' parts in index order and finalizes the Alg. 1
+// state, then the CTA sorts the row's candidate rank keys (bitonic, shared
+// memory) and emits the top K -- stage 2 without a grid round trip.
+// Optionally also writes the grid (stage1_partial_reduce).
+// ---------------------------------------------------------------------------
+template <int KP>
+__global__ void __launch_bounds__(512)
+merge_select_kernel(const uint32_t* __restrict__ in, uint32_t parts, uint64_t nstr, uint64_t len, uint32_t tiles,
+                    uint32_t vec, uint64_t B, uint32_t filled, uint32_t P, uint32_t k, float* out_v,
+                    uint32_t* out_i, float* grid_v, uint32_t* grid_i, uint32_t* status) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  const uint64_t row = blockIdx.x;
+  const uint64_t words = (uint64_t)(2 * KP + 2) * B;
+  uint32_t* stage = sm;                                                      // [parts][words]
+  uint64_t* keys = reinterpret_cast<uint64_t*>(sm + ((parts * words + 3) & ~3ull));  // [P]
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(in + row * parts * words);
+    uint4* dst = reinterpret_cast<uint4*>(stage);
+    const uint64_t n4 = parts * words / 4;
+    for (uint64_t t = threadIdx.x; t < n4; t += blockDim.x) dst[t] = src[t];
+  }
+  for (uint32_t t = threadIdx.x; t < P; t += blockDim.x) keys[t] = ~0ull;
+  __syncthreads();
+  for (uint64_t b = threadIdx.x; b < B; b += blockDim.x) {
+    const uint64_t u = row * tiles + b / (32ull * vec);
+    const uint64_t w0 = (u * nstr) / len, w1 = ((u + 1) * nstr - 1) / len;
+    const uint32_t n = (uint32_t)(w1 - w0 + 1);
+    Summ<KP> acc;
+    load_summ<KP>(stage, B, b, acc);
+    for (uint32_t q = 1; q < n; ++q) {
+      Summ<KP> o;
+      load_summ<KP>(stage + q * words, B, b, o);
+      acc.merge_later(o);
+    }
+    float ov[KP];
+    uint32_t oi[KP];
+    acc.finalize(ov, oi);
+#pragma unroll
+    for (int kk = 0; kk < KP; ++kk) {
+      if (grid_v) {
+        grid_v[row * KP * B + (uint64_t)kk * B + b] = ov[kk];
+        grid_i[row * KP * B + (uint64_t)kk * B + b] = oi[kk];
+      }
+      if ((uint32_t)kk < filled) keys[(uint64_t)kk * B + b] = rank_key_bits(__float_as_uint(ov[kk]), oi[kk]);
+    }
+  }
+  __syncthreads();
+  if (*status & ATKG_FLAG_NAN) return;  // the reference rejects NaN before ranking
+  block_bitonic_sort(keys, P);
+  for (uint32_t t = threadIdx.x; t < k; t += blockDim.x) {
+    out_v[row * k + t] = __uint_as_float(key_value_bits(keys[t]));
+    out_i[row * k + t] = (uint32_t)keys[t];
+  }
 }
 
 }  // namespace atkg
