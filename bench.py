@@ -339,7 +339,7 @@ def main():
     peak, peak_src = peaks()
     alg_bytes = rows * n * esz + rows * b * kp * 8
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
-    roof = {"kernel": "stage1_segments_kernel", "bound": "hbm", "achieved": round(achieved, 1),
+    roof = {"kernel": "stage1_flat_kernel", "bound": "hbm", "achieved": round(achieved, 1),
             "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "traffic": traffic_from_profiles(args.config), "alg_bytes_per_launch": alg_bytes,
             "launch_ms": round(kern_ms, 5), "share_of_step": round(kern_ms / ms_step, 4)}

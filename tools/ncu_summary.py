@@ -33,7 +33,7 @@ def details(rep):
 
 
 def raw(rep):
-    r = ncu_csv(rep, "--page", "raw")
+    r = ncu_csv(rep, "--page", "raw", "--print-units", "base")
     hdr, vals = r[0], r[2] if len(r) > 2 else r[1]
     return dict(zip(hdr, vals))
 
