@@ -114,7 +114,10 @@ bool kp_specialised(uint32_t kp) { return (kp >= 1 && kp <= 8) || kp == 16; }
 #define ATKG_FLAT_W 4
 #endif
 constexpr int kFlatSlots = ATKG_SLOTS;  // TMA ring slots per warp
-constexpr int kFlatRows = 8;            // stride-rows per ring slot
+#ifndef ATKG_CR
+#define ATKG_CR 8
+#endif
+constexpr int kFlatRows = ATKG_CR;       // stride-rows per ring slot
 constexpr int kFlatWarps = ATKG_FLAT_W; // warps per CTA (independent)
 constexpr int kLogCap = ATKG_LOGC;      // log entries per (lane, bucket)
 // lanes own V adjacent buckets; fewer for long lists to bound registers
@@ -128,7 +131,7 @@ constexpr int flat_vec(int kp, int esz = 4) {
 }
 // stride-rows sampled for the starting threshold of every piece
 #ifndef ATKG_Q0
-#define ATKG_Q0 16
+#define ATKG_Q0 48
 #endif
 constexpr int flat_q0(int kp) { return kp <= 2 ? ATKG_Q0 : ATKG_Q0 / 2 * kp; }
 

@@ -679,6 +679,9 @@ stage1_flat_kernel(FlatArgs a) {
   for (int q = 0; q < NS - 1; ++q) issue_next();
 
   uint32_t nan = 0;
+#ifdef ATKG_COUNT_LOG
+  uint32_t dbg_logged = 0, dbg_taken = 0, dbg_flushes = 0;
+#endif
   uint64_t F = F0;  // consumer position
   uint32_t c = 0;   // chunks consumed
   while (F < F1) {
@@ -760,6 +763,10 @@ stage1_flat_kernel(FlatArgs a) {
           if (e < cnt[v]) {
             const float x = logv[(v * LOGC + e) * 32 + lane];
             const uint32_t jj = logj[(v * LOGC + e) * 32 + lane];
+#ifdef ATKG_COUNT_LOG
+            dbg_logged++;
+            if (!(s[v].full() && x < s[v].v[KP - 1])) dbg_taken++;
+#endif
             s[v].push(x, ioff + v + jj * Bu, nan);
           }
         }
@@ -805,7 +812,12 @@ stage1_flat_kernel(FlatArgs a) {
       bool need = false;
 #pragma unroll
       for (int v = 0; v < V; ++v) need |= ptr[v] > sv0 + (uint32_t)(v * LOGC + (LOGC - CR - 1)) * 128;
-      if (__any_sync(0xffffffffu, need)) flush();
+      if (__any_sync(0xffffffffu, need)) {
+#ifdef ATKG_COUNT_LOG
+        dbg_flushes++;
+#endif
+        flush();
+      }
     }
     flush();
     // part index of this piece within its unit
@@ -820,6 +832,11 @@ stage1_flat_kernel(FlatArgs a) {
     }
   }
   if (nan) atomicOr(a.status, ATKG_FLAG_NAN);
+#ifdef ATKG_COUNT_LOG
+  atomicAdd(a.status + 1, dbg_logged);
+  atomicAdd(a.status + 2, dbg_taken);
+  if (lane == 0) atomicAdd(a.status + 3, dbg_flushes);
+#endif
 }
 
 template <typename T, int KP, int V, int W, int NS, int CR, int LOGC>
