@@ -15,6 +15,7 @@
 #include "../../include/atkg.h"
 #include "host_common.hpp"
 #include "radix.cuh"
+#include "rowres.cuh"
 #include "stage1.cuh"
 #include "stage2.cuh"
 
@@ -365,11 +366,80 @@ void run_merge(const S1Plan& pl, uint32_t kp, const uint32_t* ws, uint64_t rows,
   }
 }
 
+// ---------------------------------------------------------------------------
+// row-resident path (rowres.cuh) for rows that fit in shared memory
+// ---------------------------------------------------------------------------
+struct RowPlan {
+  bool ok = false;
+  uint32_t R = 1, TPR = 32, P = 2;
+  size_t smem = 0;
+};
+RowPlan plan_rowres(int dtype, const void* in, uint64_t n, uint64_t B, uint32_t kp) {
+  RowPlan rp;
+  const uint64_t esz = dtype == ATKG_BF16 ? 2 : 4, E = 4 / esz;
+  const uint64_t row_bytes = n * esz;
+  if (!kp_specialised(kp) || env_u64("ATKG_NO_ROWRES", 0)) return rp;
+  if (row_bytes > 64 * 1024 || row_bytes % 16 != 0 || reinterpret_cast<uintptr_t>(in) % 16 != 0) return rp;
+  if (B % E != 0 || n / B > 4096) return rp;
+  const uint64_t filled = std::min<uint64_t>(kp, n / B) * B;
+  rp.P = next_pow2(filled);
+  if (rp.P > 4096) return rp;
+  const uint64_t W = B / E;
+  rp.TPR = static_cast<uint32_t>(std::min<uint64_t>(256, (W + 31) / 32 * 32));
+  const size_t key_bytes = esz == 2 ? 4 : 8;  // bf16 rows use 32-bit rank keys
+  const size_t per_row = ((row_bytes + 127) & ~127ull) + (size_t)rp.P * key_bytes +
+                         (size_t)E * kRowLog * rp.TPR * 4;
+  rp.R = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(256 / rp.TPR, (96 * 1024) / per_row)));
+  rp.smem = rp.R * per_row;
+  rp.ok = true;
+  return rp;
+}
+template <typename T, int KP, int WN>
+void launch_rowres_wn(const RowPlan& rp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t k,
+                      float* ov, uint32_t* oi, float* gv, uint32_t* gi, uint32_t* status, cudaStream_t st) {
+  auto kern = row_resident_kernel<T, KP, WN>;
+  static size_t attr = 0;
+  if (attr < rp.smem) {
+    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rp.smem));
+    attr = rp.smem;
+  }
+  const uint32_t filled = (uint32_t)std::min<uint64_t>(KP, n / B);
+  g_prof.bracket_begin(st);
+  kern<<<static_cast<unsigned>(ceil_div(rows, rp.R)), rp.R * rp.TPR, rp.smem, st>>>(
+      static_cast<const T*>(in), rows, (uint32_t)n, (uint32_t)B, rp.R, k, filled, rp.P, ov, oi, gv, gi, status);
+  check_launch();
+  g_prof.bracket_end(st);
+}
+template <typename T, int KP>
+void launch_rowres(const RowPlan& rp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t k,
+                   float* ov, uint32_t* oi, float* gv, uint32_t* gi, uint32_t* status, cudaStream_t st) {
+  // register sort by one warp when the row's candidates are 256..1024 keys
+  switch (ov ? rp.P : 0u) {
+    case 256: launch_rowres_wn<T, KP, 8>(rp, in, rows, n, B, k, ov, oi, gv, gi, status, st); break;
+    case 512: launch_rowres_wn<T, KP, 16>(rp, in, rows, n, B, k, ov, oi, gv, gi, status, st); break;
+    case 1024: launch_rowres_wn<T, KP, 32>(rp, in, rows, n, B, k, ov, oi, gv, gi, status, st); break;
+    default: launch_rowres_wn<T, KP, 0>(rp, in, rows, n, B, k, ov, oi, gv, gi, status, st); break;
+  }
+}
+void run_rowres(int dtype, const RowPlan& rp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
+                uint32_t k, float* ov, uint32_t* oi, float* gv, uint32_t* gi, uint32_t* status, cudaStream_t st) {
+  if (dtype == ATKG_BF16) {
+    ATKG_KP_SWITCH(kp, (launch_rowres<__nv_bfloat16, K_>(rp, in, rows, n, B, k, ov, oi, gv, gi, status, st)));
+  } else {
+    ATKG_KP_SWITCH(kp, (launch_rowres<float, K_>(rp, in, rows, n, B, k, ov, oi, gv, gi, status, st)));
+  }
+}
+
 // stage 1 into a grid (grid_stride elements between rows)
 void run_stage1_grid(int dtype, const void* in, uint64_t rows, const atkg_params& p, float* gv, uint32_t* gi,
                      uint64_t gstride, void* ws, uint32_t* status, cudaStream_t st) {
   const uint64_t B = p.num_buckets;
   const uint32_t kp = p.local_k;
+  const RowPlan rp = plan_rowres(dtype, in, p.n, B, kp);
+  if (rp.ok && gstride == kp * B) {
+    run_rowres(dtype, rp, in, rows, p.n, B, kp, 0, nullptr, nullptr, gv, gi, status, st);
+    return;
+  }
   const S1Plan pl = plan_stage1(dtype, in, rows, p.n, p.n, B, kp);
   if (pl.kind == S1Plan::kGeneric) {
     if (gstride != kp * B) throw Unsupported("generic stage 1 needs a dense grid");
@@ -642,6 +712,12 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     float* gv = reinterpret_cast<float*>(w);
     uint32_t* gi = reinterpret_cast<uint32_t*>(w + rows * gstride * 4);
     w += grid_bytes(rows, *p);
+    const RowPlan rp = plan_rowres(dtype, d_in, p->n, p->num_buckets, p->local_k);
+    if (rp.ok) {  // row-resident: stage 1 + stage 2 in one kernel
+      run_rowres(dtype, rp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,
+                 nullptr, nullptr, d_status, st);
+      return;
+    }
     if (fused_tail_ok(pl, *p)) {
       // stage 1 summaries, then one fused merge + stage-2 kernel per row
       run_stage1_summaries(dtype, pl, d_in, rows, p->n, p->num_buckets, p->local_k, 0, s1ws, d_status, st);

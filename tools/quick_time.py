@@ -20,6 +20,8 @@ cfgs = {
  "C3": (8192, 14336, 128, 4, 287, "bf16"),
  "C3k1": (8192, 14336, 3584, 1, 287, "bf16"),
  "C3k8": (8192, 14336, 128, 8, 287, "bf16"),
+ "C3k2": (8192, 14336, 512, 2, 287, "bf16"),
+ "C3r99": (8192, 14336, 256, 4, 287, "bf16"),
  "C5": (1, 1 << 30, 256, 8, 1024, "f32"),
 }
 def main():
