@@ -387,17 +387,20 @@ RowPlan plan_rowres(int dtype, const void* in, uint64_t n, uint64_t B, uint32_t 
   const uint64_t W = B / E;
   rp.TPR = static_cast<uint32_t>(std::min<uint64_t>(256, (W + 31) / 32 * 32));
   const size_t key_bytes = esz == 2 ? 4 : 8;  // bf16 rows use 32-bit rank keys
-  const size_t per_row = ((row_bytes + 127) & ~127ull) + (size_t)rp.P * key_bytes +
-                         (size_t)E * kRowLog * rp.TPR * 4;
+  // keys (+ k more as the select scratch for large P) | pass-2 logs (also the
+  // select histogram)
+  const size_t keys = (size_t)(rp.P + (rp.P > 512 ? rp.P : 0)) * key_bytes;  // (P > 512: select scratch)
+  const size_t logs = std::max<size_t>((size_t)E * row_slots_max(kp) * rp.TPR * 4, 264 * 4);
+  const size_t per_row = ((row_bytes + 127) & ~127ull) + keys + logs;
   rp.R = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(256 / rp.TPR, (96 * 1024) / per_row)));
   rp.smem = rp.R * per_row;
   rp.ok = true;
   return rp;
 }
-template <typename T, int KP, int WN>
-void launch_rowres_wn(const RowPlan& rp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t k,
-                      float* ov, uint32_t* oi, float* gv, uint32_t* gi, uint32_t* status, cudaStream_t st) {
-  auto kern = row_resident_kernel<T, KP, WN>;
+template <typename T, int KP>
+void launch_rowres(const RowPlan& rp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t k,
+                   float* ov, uint32_t* oi, float* gv, uint32_t* gi, uint32_t* status, cudaStream_t st) {
+  auto kern = row_resident_kernel<T, KP>;
   static size_t attr = 0;
   if (attr < rp.smem) {
     CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rp.smem));
@@ -409,17 +412,6 @@ void launch_rowres_wn(const RowPlan& rp, const void* in, uint64_t rows, uint64_t
       static_cast<const T*>(in), rows, (uint32_t)n, (uint32_t)B, rp.R, k, filled, rp.P, ov, oi, gv, gi, status);
   check_launch();
   g_prof.bracket_end(st);
-}
-template <typename T, int KP>
-void launch_rowres(const RowPlan& rp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t k,
-                   float* ov, uint32_t* oi, float* gv, uint32_t* gi, uint32_t* status, cudaStream_t st) {
-  // register sort by one warp when the row's candidates are 256..1024 keys
-  switch (ov ? rp.P : 0u) {
-    case 256: launch_rowres_wn<T, KP, 8>(rp, in, rows, n, B, k, ov, oi, gv, gi, status, st); break;
-    case 512: launch_rowres_wn<T, KP, 16>(rp, in, rows, n, B, k, ov, oi, gv, gi, status, st); break;
-    case 1024: launch_rowres_wn<T, KP, 32>(rp, in, rows, n, B, k, ov, oi, gv, gi, status, st); break;
-    default: launch_rowres_wn<T, KP, 0>(rp, in, rows, n, B, k, ov, oi, gv, gi, status, st); break;
-  }
 }
 void run_rowres(int dtype, const RowPlan& rp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
                 uint32_t k, float* ov, uint32_t* oi, float* gv, uint32_t* gi, uint32_t* status, cudaStream_t st) {

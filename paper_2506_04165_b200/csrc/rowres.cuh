@@ -112,6 +112,73 @@ __device__ __forceinline__ float key32_value_bf16(uint32_t key) {
   return __uint_as_float(h << 16);
 }
 
+
+// Moves the k smallest of P unique keys to s[0..k) (unordered) and pads
+// s[k..next_pow2(k)) with ~0.  MSB-first 8-bit radix select with a shared
+// histogram (`scr` = 264 words per row group); every group runs the same
+// schedule, so the __syncthreads are uniform.
+template <typename K>
+__device__ __forceinline__ void group_select_front(K* s, uint32_t P, uint32_t k, uint32_t t, uint32_t nt,
+                                                   uint32_t* scr) {
+  constexpr int BITS = sizeof(K) * 8;
+  uint32_t* hist = scr;        // 256 bins
+  uint32_t* ctl = scr + 256;   // [0] digit, [1] remaining k, [2] counter
+  K prefix = 0, mask = 0;
+  uint32_t krem = k;
+  for (int shift = BITS - 8; shift >= 0; shift -= 8) {
+    for (uint32_t q = t; q < 256; q += nt) hist[q] = 0;
+    __syncthreads();
+    for (uint32_t q = t; q < P; q += nt) {
+      const K key = s[q];
+      if ((key & mask) == prefix) atomicAdd(&hist[(uint32_t)(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (t < 32) {  // warp scan: lane owns bins [8 t, 8 t + 8)
+      uint32_t c[8], tot = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { c[q] = hist[t * 8 + q]; tot += c[q]; }
+      uint32_t incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((int)t >= o) incl += y;
+      }
+      const uint32_t excl = incl - tot;
+      if (excl < krem && krem <= incl) {
+        uint32_t acc = excl;
+        int d = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (d == 0 && acc + c[q] >= krem) { d = q + 1; break; }
+          acc += c[q];
+        }
+        ctl[0] = t * 8 + (d - 1);
+        ctl[1] = krem - acc;
+      }
+    }
+    __syncthreads();
+    prefix |= (K)ctl[0] << shift;
+    mask |= (K)0xff << shift;
+    krem = ctl[1];
+    __syncthreads();
+  }
+  // prefix is now the k-th smallest key; gather keys <= it (exactly k)
+  if (t == 0) ctl[2] = 0;
+  __syncthreads();
+  for (uint32_t q = t; q < P; q += nt) {
+    const K key = s[q];
+    if (key <= prefix) {
+      const uint32_t slot = atomicAdd(&ctl[2], 1u);
+      s[P + slot] = key;
+    }
+  }
+  __syncthreads();
+  uint32_t kp2 = 2;
+  while (kp2 < k) kp2 <<= 1;
+  for (uint32_t q = t; q < kp2; q += nt) s[q] = q < k ? s[P + q] : (K)~(K)0;
+  __syncthreads();
+}
+
 template <typename T>
 struct WordNet;  // packed top-KP values of the E buckets of one 32-bit word
 
@@ -137,6 +204,18 @@ struct WordNet<__nv_bfloat16> {
   __device__ __forceinline__ static float lane(uint32_t w, int e) {
     return __uint_as_float(e ? (w & 0xffff0000u) : (w << 16));
   }
+  // per-half !(x < v*) (NaN included) as two predicates from one HSETP2
+  __device__ __forceinline__ static void hit(uint32_t w, uint32_t vs, bool (&h)[2]) {
+    uint32_t lo, hi;
+    asm("{\n\t.reg .pred p, q;\n\t"
+        "setp.geu.bf16x2 p|q, %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t"
+        "selp.u32 %1, 1, 0, q;\n\t}"
+        : "=r"(lo), "=r"(hi)
+        : "r"(w), "r"(vs));
+    h[0] = lo != 0;
+    h[1] = hi != 0;
+  }
 };
 
 template <>
@@ -159,14 +238,20 @@ struct WordNet<float> {
     }
   }
   __device__ __forceinline__ static float lane(uint32_t w, int) { return __uint_as_float(w); }
+  __device__ __forceinline__ static void hit(uint32_t w, uint32_t vs, bool (&h)[1]) {
+    h[0] = !(__uint_as_float(w) < __uint_as_float(vs));
+  }
 };
 
 // CTA = R row groups of TPR threads (TPR a multiple of 32).
 // smem: R rows of n elements | R x P candidate keys | R x E x LOGC x TPR
 // pass-2 position logs.
-constexpr int kRowLog = 8;  // positions logged per (thread, bucket) in pass 2
+// positions logged per (thread, bucket) in pass 2: K' plus room for ties
+template <int KP>
+constexpr int row_log_cap() { return KP + 6; }
+constexpr int row_slots_max(int kp) { return kp + 7; }  // + a dump slot the cursor saturates on
 
-template <typename T, int KP, int WN>
+template <typename T, int KP>
 __global__ void __launch_bounds__(256)
 row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_t B, uint32_t R, uint32_t k,
                     uint32_t filled, uint32_t P, float* out_v, uint32_t* out_i, float* grid_v, uint32_t* grid_i,
@@ -184,8 +269,9 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
   const uint32_t nrows = (uint32_t)umin64(R, rows - row0);
   const uint32_t row_bytes = n * sizeof(T);
   const uint32_t row_stride_b = (row_bytes + 127) & ~127u;
+  const uint32_t key_stride = P > 512u ? 2 * P : P;  // + select scratch
   Key* keys = reinterpret_cast<Key*>(smem_raw + (size_t)R * row_stride_b);
-  uint32_t* logs = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(keys) + (size_t)R * P * sizeof(Key));
+  uint32_t* logs = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(keys) + (size_t)R * key_stride * sizeof(Key));
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar, 1);
     ptx::fence_mbar_init();
@@ -194,7 +280,7 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
     for (uint32_t r = 0; r < nrows; ++r)
       ptx::bulk_g2s(smem_raw + r * row_stride_b, in + (row0 + r) * n, row_bytes, &bar, pol);
   }
-  for (uint32_t q = threadIdx.x; q < R * P; q += blockDim.x) keys[q] = (Key)~(Key)0;
+  for (uint32_t q = threadIdx.x; q < R * key_stride; q += blockDim.x) keys[q] = (Key)~(Key)0;
   __syncthreads();
   ptx::mbar_wait(&bar, 0);
 
@@ -203,8 +289,11 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
   const uint32_t* words = reinterpret_cast<const uint32_t*>(smem_raw + g * row_stride_b);
   const uint32_t W = B / E;      // words per stride-row
   const uint32_t nstr = n / B;   // stride-rows
-  Key* rkeys = keys + (uint64_t)g * P;
-  uint32_t* mylog = logs + (uint64_t)g * E * kRowLog * TPR + t;  // [e][q][TPR]
+  Key* rkeys = keys + (uint64_t)g * key_stride;
+  constexpr int kRowLog = row_log_cap<KP>();
+  constexpr int kRowSlots = kRowLog + 1;
+  const uint32_t log_stride = E * kRowSlots * TPR > 264u ? E * kRowSlots * TPR : 264u;
+  uint32_t* mylog = logs + (uint64_t)g * log_stride + t;  // [e][slot][TPR]
   uint32_t nan = 0;
   for (uint32_t p = t; row_ok && p < W; p += TPR) {
     // pass 1: exact K'-th largest values of the E buckets of word column p
@@ -218,27 +307,42 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
     uint32_t cnt[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) cnt[e] = 0;
+    const uint32_t vs = net[KP - 1];  // packed v* of the word's buckets
+    // per-bucket log cursors (bytes); they saturate at slot kRowLog, which
+    // marks an overflow (heavy ties) and sends the bucket to the full replay
+    uint32_t lp[E], lend[E];
+    const uint32_t lbase = (uint32_t)__cvta_generic_to_shared(mylog);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      lp[e] = lbase + e * kRowSlots * TPR * 4;
+      lend[e] = lp[e] + kRowLog * TPR * 4;  // the dump slot
+    }
+    const uint32_t lstride = TPR * 4;
     for (uint32_t j = 0; j < nstr; ++j) {
-      const uint32_t w = words[j * W + p];
+      bool h[E];
+      Net::hit(words[j * W + p], vs, h);
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const float x = Net::lane(w, e);
-        const bool h = !(x < vstar[e]);
-        if (h && cnt[e] < (uint32_t)kRowLog) mylog[(e * kRowLog + cnt[e]) * TPR] = j;
-        cnt[e] += h ? 1u : 0u;
+        if (h[e]) {
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(lp[e]), "r"(j) : "memory");
+          lp[e] += lstride;
+        }
+        lp[e] = lp[e] < lend[e] ? lp[e] : lend[e];
       }
     }
+#pragma unroll
+    for (int e = 0; e < E; ++e) cnt[e] = (lp[e] - (lbase + e * kRowSlots * TPR * 4)) / lstride;
     // pass 2b: exact summaries of the logged elements (S* = {x >= v*});
-    // a bucket with more than kRowLog such elements (heavy ties) replays
+    // a bucket with kRowLog or more such elements (heavy ties) replays
     // its whole stride-row sequence instead
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       Summ<KP> s;
       s.clear();
       const uint32_t b = p * E + e;
-      if (cnt[e] <= (uint32_t)kRowLog) {
+      if (cnt[e] < (uint32_t)kRowLog) {
         for (uint32_t q = 0; q < cnt[e]; ++q) {
-          const uint32_t j = mylog[(e * kRowLog + q) * TPR];
+          const uint32_t j = mylog[(e * kRowSlots + q) * TPR];
           s.push(Net::lane(words[j * W + p], e), j * B + b, nan);
         }
       } else {
@@ -266,19 +370,36 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
   if (nan) atomicOr(status, ATKG_FLAG_NAN);
   if (!out_v) return;  // stage-1 only (uniform across the CTA)
   __syncthreads();
-  if (WN > 0 && P == 32u * WN) {
-    // one warp of the row group sorts the row's P keys in registers
+  uint32_t nsort = P;
+  if (P > 512u) {
+    // large candidate sets: radix-select the k smallest (unique) keys into
+    // the front, then sort only those
+    group_select_front<Key>(rkeys, P, k, t, TPR, logs + (uint64_t)g * log_stride);
+    nsort = 2;
+    while (nsort < k) nsort <<= 1;
+  }
+  if (nsort == 512u || nsort == 256u) {
+    // one warp of the row group sorts in registers
     if (row_ok && t < 32) {
-      Key kk[WN > 0 ? WN : 1];
+      if (nsort == 512u) {
+        Key kk[16];
 #pragma unroll
-      for (int r = 0; r < WN; ++r) kk[r] = rkeys[t * WN + r];
-      warp_bitonic_sort<Key, (WN > 0 ? WN : 1)>(kk, (int)t);
+        for (int r = 0; r < 16; ++r) kk[r] = rkeys[t * 16 + r];
+        warp_bitonic_sort<Key, 16>(kk, (int)t);
 #pragma unroll
-      for (int r = 0; r < WN; ++r) rkeys[t * WN + r] = kk[r];
+        for (int r = 0; r < 16; ++r) rkeys[t * 16 + r] = kk[r];
+      } else {
+        Key kk[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) kk[r] = rkeys[t * 8 + r];
+        warp_bitonic_sort<Key, 8>(kk, (int)t);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) rkeys[t * 8 + r] = kk[r];
+      }
     }
     __syncthreads();
   } else {
-    group_bitonic_sort<Key>(rkeys, P, t, TPR);
+    group_bitonic_sort<Key>(rkeys, nsort, t, TPR);
   }
   if (!row_ok || (*status & ATKG_FLAG_NAN)) return;
   for (uint32_t q = t; q < k; q += TPR) {
