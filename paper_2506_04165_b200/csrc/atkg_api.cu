@@ -14,6 +14,7 @@
 
 #include "../../include/atkg.h"
 #include "host_common.hpp"
+#include "internal.hpp"
 #include "radix.cuh"
 #include "rowres.cuh"
 #include "stage1.cuh"
@@ -24,40 +25,8 @@ namespace atkg {
 thread_local std::string g_last_error;
 void set_last_error(const std::string& m) { g_last_error = m; }
 
-#define CUDA_OK(x)                                                                      \
-  do {                                                                                  \
-    cudaError_t e_ = (x);                                                               \
-    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
-
 std::atomic<uint64_t> g_launches{0};
-struct Profiler {
-  bool on = false;
-  std::vector<cudaEvent_t> ev;  // pairs
-  size_t used = 0;
-  void bracket_begin(cudaStream_t st) {
-    if (!on) return;
-    if (used + 2 > ev.size()) {
-      for (int q = 0; q < 2; ++q) {
-        cudaEvent_t e;
-        CUDA_OK(cudaEventCreate(&e));
-        ev.push_back(e);
-      }
-    }
-    CUDA_OK(cudaEventRecord(ev[used], st));
-  }
-  void bracket_end(cudaStream_t st) {
-    if (!on) return;
-    CUDA_OK(cudaEventRecord(ev[used + 1], st));
-    used += 2;
-  }
-};
 Profiler g_prof;
-
-inline void check_launch() {
-  CUDA_OK(cudaGetLastError());
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-}
 
 constexpr int kSegWarps = 8;   // warps (= segments) per stage-1 CTA
 constexpr int kPrefetch = 4;   // stride-rows per batch in the stage-1 loop
@@ -72,7 +41,7 @@ int sm_count() {
   return n;
 }
 
-uint64_t align_up(uint64_t x, uint64_t a = 256) { return (x + a - 1) / a * a; }
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 uint32_t next_pow2(uint64_t x) {
   uint32_t p = 2;
@@ -499,6 +468,20 @@ uint64_t select_ws_bytes(uint64_t rows, uint64_t count, uint32_t k) {
 void run_select(const float* vals, const uint32_t* idx, uint64_t rows, uint64_t count, uint64_t stride, uint32_t k,
                 uint64_t limit, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st) {
   const uint32_t P = next_pow2(count);
+  if (P <= 512) {  // one warp per row, keys in registers
+    const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
+    const uint32_t c32 = static_cast<uint32_t>(count);
+    if (P <= 64)
+      stage2_warp_kernel<2><<<grid, 256, 0, st>>>(vals, idx, rows, c32, stride, k, limit, ov, oi, status);
+    else if (P <= 128)
+      stage2_warp_kernel<4><<<grid, 256, 0, st>>>(vals, idx, rows, c32, stride, k, limit, ov, oi, status);
+    else if (P <= 256)
+      stage2_warp_kernel<8><<<grid, 256, 0, st>>>(vals, idx, rows, c32, stride, k, limit, ov, oi, status);
+    else
+      stage2_warp_kernel<16><<<grid, 256, 0, st>>>(vals, idx, rows, c32, stride, k, limit, ov, oi, status);
+    check_launch();
+    return;
+  }
   if (P <= kMaxSortKeys) {
     static bool attr = false;
     if (!attr) {

@@ -1,0 +1,61 @@
+// internal.hpp -- host-side helpers shared by the library's translation
+// units (atkg_api.cu, fused_gemm.cu); not part of the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "host_common.hpp"
+
+namespace atkg {
+
+#define CUDA_OK(x)                                                                           \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// launch counter (atkg_launch_count) and the stage-1 event brackets
+// (atkg_profile_begin/end)
+extern std::atomic<uint64_t> g_launches;
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // pairs
+  size_t used = 0;
+  void bracket_begin(cudaStream_t st) {
+    if (!on) return;
+    if (used + 2 > ev.size()) {
+      for (int q = 0; q < 2; ++q) {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreate(&e));
+        ev.push_back(e);
+      }
+    }
+    CUDA_OK(cudaEventRecord(ev[used], st));
+  }
+  void bracket_end(cudaStream_t st) {
+    if (!on) return;
+    CUDA_OK(cudaEventRecord(ev[used + 1], st));
+    used += 2;
+  }
+};
+extern Profiler g_prof;
+
+inline void check_launch() {
+  CUDA_OK(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+int sm_count();
+uint64_t align_up(uint64_t x, uint64_t a = 256);
+uint32_t next_pow2(uint64_t x);
+void validate(const atkg_params& p);
+uint64_t select_ws_bytes(uint64_t rows, uint64_t count, uint32_t k);
+void run_select(const float* vals, const uint32_t* idx, uint64_t rows, uint64_t count, uint64_t stride, uint32_t k,
+                uint64_t limit, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
+
+}  // namespace atkg

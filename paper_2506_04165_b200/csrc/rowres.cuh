@@ -48,57 +48,6 @@ __device__ __forceinline__ void group_bitonic_sort(K* s, uint32_t P, uint32_t t,
 }
 
 
-// ---------------------------------------------------------------------------
-// single-warp register bitonic sort, ascending, N keys per lane in
-// lane-major order (element i = lane * N + r); strides < N stay in
-// registers, larger strides exchange whole registers across lanes.
-// ---------------------------------------------------------------------------
-template <typename K>
-__device__ __forceinline__ K shfl_key(K v, int m) {
-  if constexpr (sizeof(K) == 8) {
-    const uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)v, m);
-    const uint32_t hi = __shfl_xor_sync(0xffffffffu, (uint32_t)(v >> 32), m);
-    return ((uint64_t)hi << 32) | lo;
-  } else {
-    return __shfl_xor_sync(0xffffffffu, v, m);
-  }
-}
-
-template <typename K, int N>
-__device__ __forceinline__ void warp_bitonic_sort(K (&k)[N], int lane) {
-  constexpr int TOT = 32 * N;
-#pragma unroll
-  for (int size = 2; size <= TOT; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      if (stride >= N) {
-        const int m = stride / N;  // partner lane distance
-        const bool low = (lane & m) == 0;
-#pragma unroll
-        for (int r = 0; r < N; ++r) {
-          const int i = lane * N + r;
-          const bool asc = (i & size) == 0;
-          const K o = shfl_key(k[r], m);
-          const K mn = k[r] < o ? k[r] : o, mx = k[r] < o ? o : k[r];
-          k[r] = (low == asc) ? mn : mx;
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < N; ++r) {
-          if ((r & stride) == 0) {
-            const int i = lane * N + r;
-            const bool asc = (i & size) == 0;
-            const K a = k[r], b = k[r + stride];
-            const bool sw = (a > b) == asc;
-            k[r] = sw ? b : a;
-            k[r + stride] = sw ? a : b;
-          }
-        }
-      }
-    }
-  }
-}
-
 // bf16 candidate -> 32-bit rank key (value desc, index asc; -0.0 == +0.0)
 __device__ __forceinline__ uint32_t rank_key32_bf16(uint32_t f32bits, uint32_t index) {
   uint32_t h = f32bits >> 16;

@@ -73,4 +73,103 @@ __global__ void stage2_bitonic_kernel(const float* __restrict__ vals, const uint
   }
 }
 
+// ---------------------------------------------------------------------------
+// single-warp register bitonic sort, ascending, N keys per lane in
+// lane-major order (element i = lane * N + r); strides < N stay in
+// registers, larger strides exchange whole registers across lanes.
+// ---------------------------------------------------------------------------
+template <typename K>
+__device__ __forceinline__ K shfl_key(K v, int m) {
+  if constexpr (sizeof(K) == 8) {
+    const uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)v, m);
+    const uint32_t hi = __shfl_xor_sync(0xffffffffu, (uint32_t)(v >> 32), m);
+    return ((uint64_t)hi << 32) | lo;
+  } else {
+    return __shfl_xor_sync(0xffffffffu, v, m);
+  }
+}
+
+template <typename K, int N>
+__device__ __forceinline__ void warp_bitonic_sort(K (&k)[N], int lane) {
+  constexpr int TOT = 32 * N;
+#pragma unroll
+  for (int size = 2; size <= TOT; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= N) {
+        const int m = stride / N;  // partner lane distance
+        const bool low = (lane & m) == 0;
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          const int i = lane * N + r;
+          const bool asc = (i & size) == 0;
+          const K o = shfl_key(k[r], m);
+          const K mn = k[r] < o ? k[r] : o, mx = k[r] < o ? o : k[r];
+          k[r] = (low == asc) ? mn : mx;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          if ((r & stride) == 0) {
+            const int i = lane * N + r;
+            const bool asc = (i & size) == 0;
+            const K a = k[r], b = k[r + stride];
+            const bool sw = (a > b) == asc;
+            k[r] = sw ? b : a;
+            k[r + stride] = sw ? a : b;
+          }
+        }
+      }
+    }
+  }
+}
+
+
+// one warp per row for count <= 32*N candidates: keys in registers (lane-major,
+// element i = lane*N + r), warp bitonic sort, first k emitted
+template <int N>
+__global__ void __launch_bounds__(256) stage2_warp_kernel(const float* __restrict__ vals,
+                                                          const uint32_t* __restrict__ idx, uint64_t rows,
+                                                          uint32_t count, uint64_t stride, uint32_t k,
+                                                          uint64_t index_limit, float* out_v, uint32_t* out_i,
+                                                          uint32_t* status) {
+  // no early exits: every lane of the warp reaches the shuffles, so they
+  // compile to plain SHFL (no collective fix-up code)
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t row0 = (uint64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const bool live = row0 < rows;
+  const uint64_t row = live ? row0 : rows - 1;
+  const float* vr = vals + row * stride;
+  const uint32_t* ir = idx + row * stride;
+  uint64_t key[N];
+  uint32_t mine = 0, bad = 0;
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    const uint32_t c = lane * N + r;
+    key[r] = ~0ull;
+    if (c < count) {
+      const float v = vr[c];
+      const uint32_t ix = ir[c];
+      bad |= (v != v);
+      if ((uint64_t)ix < index_limit) { key[r] = rank_key_bits(__float_as_uint(v), ix); ++mine; }
+    }
+  }
+  const bool any_bad = __any_sync(0xffffffffu, bad);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  warp_bitonic_sort<uint64_t, N>(key, (int)lane);
+  if (!live) return;
+  if (any_bad || mine < k) {
+    if (lane == 0) atomicOr(status, any_bad ? ATKG_FLAG_NAN : kFlagFew);
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    const uint32_t c = lane * N + r;
+    if (c < k) {
+      out_v[row * k + c] = __uint_as_float(key_value_bits(key[r]));
+      out_i[row * k + c] = (uint32_t)key[r];
+    }
+  }
+}
 }  // namespace atkg

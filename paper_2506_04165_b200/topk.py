@@ -440,3 +440,64 @@ def summary_merge_top_k_device(summaries: "torch.Tensor", params: AlgoParams, wa
     if status is None:
         _check_device_status(st, dev)
     return (ov, oi, gv, gi) if want_grid else (ov, oi)
+
+
+# ---------------------------------------------------------------------------
+# C4: tcgen05 GEMM with stage 1 in the epilogue (mips_fused, mips.cpp:138-193)
+# ---------------------------------------------------------------------------
+def _check_gemm_operands(x, w_t):
+    if x.dtype != torch.bfloat16 or w_t.dtype != torch.bfloat16:
+        raise ValueError("GEMM operands must be bfloat16")
+    if x.dim() != 2 or w_t.dim() != 2 or x.shape[1] != w_t.shape[1]:
+        raise ValueError("x must be [M, Kd] and w_t [N, Kd]")
+    return x.contiguous(), w_t.contiguous()
+
+
+def gemm_bf16_device(x: "torch.Tensor", w_t: "torch.Tensor", out=None) -> "torch.Tensor":
+    """fp32 scores = x[M,Kd] . w_t[N,Kd]^T on the tcgen05 tensor cores."""
+    x, w_t = _check_gemm_operands(x, w_t)
+    m, kd = x.shape
+    n = w_t.shape[0]
+    dev = x.device
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float32, device=dev)
+    check(lib.atkg_gemm_bf16(x.data_ptr(), w_t.data_ptr(), m, kd, n, out.data_ptr(), _stream_ptr(dev)))
+    return out
+
+
+def fused_workspace_bytes(m: int, kdim: int, params: AlgoParams) -> int:
+    out = C.c_size_t()
+    p = params.c()
+    check(lib.atkg_fused_workspace_size(m, kdim, C.byref(p), C.byref(out)))
+    return out.value
+
+
+def fused_gemm_top_k_device(x: "torch.Tensor", w_t: "torch.Tensor", params: AlgoParams,
+                            scores: "torch.Tensor | None" = None, status=None, out=None):
+    """Approximate top-K of every row of x . w_t^T without materialising the
+    scores (params.n == N).  `scores` (an [M, N] f32 tensor) optionally
+    receives the exact fp32 scores the epilogue consumed, for oracle replay."""
+    params.validate()
+    x, w_t = _check_gemm_operands(x, w_t)
+    m, kd = x.shape
+    if w_t.shape[0] != params.n:
+        raise ValueError("w_t must have params.n rows")
+    dev = x.device
+    k = params.global_k
+    if out is None:
+        vals = torch.empty((m, k), dtype=torch.float32, device=dev)
+        idx = torch.empty((m, k), dtype=torch.int32, device=dev)
+    else:
+        vals, idx = out
+    if scores is not None and (scores.dtype != torch.float32 or tuple(scores.shape) != (m, params.n)
+                               or not scores.is_contiguous()):
+        raise ValueError("scores must be a contiguous float32 [M, N] tensor")
+    p = params.c()
+    ws = workspace(fused_workspace_bytes(m, kd, params), dev)
+    st = status if status is not None else _status(dev)
+    check(lib.atkg_fused_gemm_top_k(x.data_ptr(), w_t.data_ptr(), m, kd, C.byref(p), vals.data_ptr(),
+                                    idx.data_ptr(), scores.data_ptr() if scores is not None else None,
+                                    ws.data_ptr(), ws.numel(), st.data_ptr(), _stream_ptr(dev)))
+    if status is None:
+        _check_device_status(st, dev)
+    return vals, idx
