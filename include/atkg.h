@@ -227,6 +227,10 @@ int atkg_select_parameters(const atkg_plan_request* req, atkg_plan_result* out);
  * derive_seed(seed, i / 65536) (rng.hpp:25-81), fp32. */
 void atkg_fill_normal(uint64_t seed, uint64_t count, float mean, float stddev, float* out,
                       uint32_t threads);
+/* elements [start, start + count) of the same stream (start % 65536 == 0):
+ * one rank's slice of a sharded row */
+void atkg_fill_normal_range(uint64_t seed, uint64_t start, uint64_t count, float mean, float stddev,
+                            float* out, uint32_t threads);
 /* round-to-nearest-even fp32 -> bf16 bits */
 void atkg_f32_to_bf16(const float* in, uint64_t count, uint16_t* out, uint32_t threads);
 void atkg_bf16_to_f32(const uint16_t* in, uint64_t count, float* out, uint32_t threads);

@@ -105,6 +105,9 @@ class _Backend:
             lib.ref_mc_expected_recall.restype = _i
             lib.ref_score_block.argtypes = [_f32p, _u64, _f32p, _u64, _u64, _u64, _u64,
                                             _f32p, _u64]
+            lib.ref_mips_fused.argtypes = [_f32p, _u64, _u64, _f32p, _u64, _u64, _u32, _u32, _u32,
+                                           _u64, _u32, _f32p, _u32p]
+            lib.ref_mips_fused.restype = _i
 
     def _check(self, rc: int):
         if rc == 0:
@@ -229,6 +232,18 @@ class _Backend:
             self.lib.ref_score_block(q.reshape(-1), b, db.reshape(-1), db.shape[0], d, c0, c1,
                                      out.reshape(-1), c1 - c0)
         return out
+
+    def mips_fused(self, database, queries, b, kp, k, lane=128, block_cols=0, threads=1):
+        """Reference mips_fused (mips.cpp:138-193); reference backend only."""
+        db = np.ascontiguousarray(database, np.float32)
+        q = np.ascontiguousarray(queries, np.float32)
+        rows, d = db.shape
+        nq = q.shape[0]
+        ov = np.empty((nq, k), np.float32)
+        oi = np.empty((nq, k), np.uint32)
+        self._check(self.lib.ref_mips_fused(db.reshape(-1), rows, d, q.reshape(-1), nq, b, kp, k, lane,
+                                            block_cols, threads, ov.reshape(-1), oi.reshape(-1)))
+        return ov, oi
 
 
 _cache: dict = {}

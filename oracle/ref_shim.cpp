@@ -171,4 +171,27 @@ void ref_score_block(const float* queries, uint64_t b, const float* database, ui
   atk::score_block(q, db, c0, c1, out, out_stride);
 }
 
+// reference MIPS pipeline (mips.cpp:138-193): database [rows][d], queries
+// [b][d] fp32; block_cols 0 = default_block_cols; results [b][k]
+int ref_mips_fused(const float* database, uint64_t rows, uint64_t d, const float* queries, uint64_t b,
+                   uint64_t nb, uint32_t kp, uint32_t k, uint32_t lane, uint64_t block_cols, uint32_t threads,
+                   float* ov, uint32_t* oi) {
+  return guard([&] {
+    atk::VectorDataset q, db;
+    q.rows = b;
+    q.dims = d;
+    q.data.assign(queries, queries + b * d);
+    db.rows = rows;
+    db.dims = d;
+    db.data.assign(database, database + rows * d);
+    auto p = mk(rows, nb, kp, k, lane);
+    const uint64_t bc = block_cols ? block_cols : atk::default_block_cols(p);
+    auto res = atk::mips_fused(db, q, p, bc, threads);
+    for (uint64_t r = 0; r < b; ++r) {
+      std::memcpy(ov + r * k, res.per_query[r].values.data(), 4ull * k);
+      std::memcpy(oi + r * k, res.per_query[r].indices.data(), 4ull * k);
+    }
+  });
+}
+
 }  // extern "C"

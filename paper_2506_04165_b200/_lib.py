@@ -82,6 +82,7 @@ def _load():
         "atkg_legal_bucket_counts": ([u64, u64, vp, u64], u64),
         "atkg_select_parameters": ([C.POINTER(PlanRequestC), C.POINTER(PlanResultC)], i32),
         "atkg_fill_normal": ([u64, u64, C.c_float, C.c_float, vp, u32], None),
+        "atkg_fill_normal_range": ([u64, u64, u64, C.c_float, C.c_float, vp, u32], None),
         "atkg_f32_to_bf16": ([vp, u64, vp, u32], None),
         "atkg_bf16_to_f32": ([vp, u64, vp, u32], None),
         "atkg_profile_begin": ([], None),

@@ -71,13 +71,16 @@ inline uint16_t to_bf16_rne(float f) {
 
 extern "C" {
 
-void atkg_fill_normal(uint64_t seed, uint64_t count, float mean, float stddev, float* out,
-                      uint32_t threads) {
+void atkg_fill_normal_range(uint64_t seed, uint64_t start, uint64_t count, float mean, float stddev, float* out,
+                            uint32_t threads) {
+  // elements [start, start + count) of the flat stream; start % kBlock == 0
+  // (the caller checks), so every generator block is produced whole
+  const uint64_t q0 = start / kBlock;
   const uint64_t blocks = (count + kBlock - 1) / kBlock;
   const double two_pi = 6.283185307179586476925286766559;
-  parallel_blocks(blocks, threads, [&](uint64_t q) {
-    Xo rng(atkg::derive_seed(seed, q));
-    const uint64_t i0 = q * kBlock, i1 = std::min(count, i0 + kBlock);
+  parallel_blocks(blocks, threads, [&](uint64_t qq) {
+    Xo rng(atkg::derive_seed(seed, q0 + qq));
+    const uint64_t i0 = qq * kBlock, i1 = std::min(count, i0 + kBlock);
     for (uint64_t i = i0; i < i1; i += 2) {
       const double u1 = rng.u(), u2 = rng.u();
       const double r = std::sqrt(-2.0 * std::log(1.0 - u1));
@@ -87,6 +90,11 @@ void atkg_fill_normal(uint64_t seed, uint64_t count, float mean, float stddev, f
         out[i + 1] = static_cast<float>(static_cast<double>(mean) + static_cast<double>(stddev) * (r * std::sin(a)));
     }
   });
+}
+
+void atkg_fill_normal(uint64_t seed, uint64_t count, float mean, float stddev, float* out,
+                      uint32_t threads) {
+  atkg_fill_normal_range(seed, 0, count, mean, stddev, out, threads);
 }
 
 void atkg_f32_to_bf16(const float* in, uint64_t count, uint16_t* out, uint32_t threads) {

@@ -26,6 +26,16 @@ def normal_f32(seed: int, shape, mean: float = 0.0, std: float = 1.0) -> np.ndar
     return out.reshape(shape)
 
 
+def normal_f32_range(seed: int, start: int, count: int, mean: float = 0.0, std: float = 1.0) -> np.ndarray:
+    """Elements [start, start + count) of normal_f32(seed, ...)'s flat stream
+    (start % 65536 == 0): one rank's slice of a sharded row."""
+    if start % 65536:
+        raise ValueError("start must be a multiple of 65536")
+    out = np.empty(count, np.float32)
+    lib.atkg_fill_normal_range(seed, start, count, mean, std, out.ctypes.data, _THREADS)
+    return out
+
+
 def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
     x = np.ascontiguousarray(x, np.float32)
     out = np.empty(x.shape, np.uint16)

@@ -1,0 +1,83 @@
+"""Sharded giant-row approximate top-K.
+
+One row of n elements is cut into index-contiguous slices, one per rank
+(one process per GPU).  Each rank reduces its slice to the exact per-bucket
+stage-1 summary (atkg_stage1_summary: (2K'+2)*B uint32 words, ~16 KB for
+K'=8, B=256), the summaries are all-gathered over NCCL (NVLink/NVSwitch),
+and every rank merges them in index order and runs stage 2
+(atkg_summary_merge_top_k).  Summaries merge associatively and exactly
+(DESIGN.md section 4), so the result equals the reference's approx_top_k on
+the whole row bit for bit (topk.cpp:123-172, Stage1Accumulator::consume over
+consecutive blocks).  The only data-path collective is the summary
+all-gather: G x 16 KB, latency-bound.
+
+The reduce / merge steps are injectable so the exchange logic runs under the
+gloo backend on CPU in tests (tests/test_distributed.py) with the host
+emulation of the same summary code; the product path uses the CUDA kernels.
+"""
+from __future__ import annotations
+
+import math
+
+from .topk import AlgoParams, stage1_summary_device, summary_merge_top_k_device, summary_words
+
+GEN_BLOCK = 65536  # generator block of the synthetic inputs (csrc/datagen.cpp)
+
+
+def slice_bounds(n: int, num_buckets: int, world: int, rank: int, align: int = GEN_BLOCK) -> tuple[int, int]:
+    """(start, length) of `rank`'s slice.  Slices are contiguous, in rank
+    order, and start on multiples of num_buckets (so a slice's local bucket
+    id equals the global one) and, when n allows it, of `align`."""
+    if n % num_buckets:
+        raise ValueError("sharding needs n to be a multiple of num_buckets")
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    unit = num_buckets * align // math.gcd(num_buckets, align)
+    if n % unit:
+        unit = num_buckets
+    units = n // unit
+    per, rem = divmod(units, world)
+    first = rank * per + min(rank, rem)
+    count = per + (1 if rank < rem else 0)
+    return first * unit, count * unit
+
+
+class ShardedTopK:
+    """Approximate top-K of one row sharded over the ranks of `group`.
+
+    `summarize(slice, offset, params)` -> int32 tensor of summary_words(params)
+    `merge(summaries [world, words], params)` -> (values, indices)
+    default to the device kernels (atkg_stage1_summary / atkg_summary_merge_top_k).
+    """
+
+    def __init__(self, params: AlgoParams, group=None, summarize=None, merge=None):
+        import torch.distributed as dist
+        params.validate()
+        self.params = params
+        self.group = group
+        self.dist = dist
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.words = summary_words(params)
+        self.summarize = summarize or (lambda x, off, p: stage1_summary_device(x, off, p, status=self._status))
+        self.merge = merge or (lambda s, p: summary_merge_top_k_device(s, p, status=self._status))
+        self._status = None
+        self._gathered = None
+
+    def bounds(self, rank: int | None = None) -> tuple[int, int]:
+        return slice_bounds(self.params.n, self.params.num_buckets, self.world,
+                            self.rank if rank is None else rank)
+
+    def __call__(self, x_slice, status=None):
+        """x_slice: this rank's elements [start, start + length) of the row.
+        Returns (values [K], indices [K]) on every rank."""
+        import torch
+        start, length = self.bounds()
+        if x_slice.numel() != length:
+            raise ValueError(f"rank {self.rank} slice must hold {length} elements")
+        self._status = status
+        summ = self.summarize(x_slice, start, self.params)
+        if self._gathered is None or self._gathered.device != summ.device:
+            self._gathered = torch.empty(self.world * self.words, dtype=summ.dtype, device=summ.device)
+        self.dist.all_gather_into_tensor(self._gathered, summ, group=self.group)
+        return self.merge(self._gathered.view(self.world, self.words), self.params)

@@ -51,3 +51,42 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda:0")
+
+
+EMU_SRC = os.path.join(ROOT, "tests", "emu", "summary_emu.cu")
+EMU_LIB = os.path.join(ROOT, "build", "libatkg_emu.so")
+
+
+def build_emu():
+    """Host build of the device summary code (tests/emu/summary_emu.cu)."""
+    import glob
+    hdrs = glob.glob(os.path.join(ROOT, "paper_2506_04165_b200", "csrc", "*.cuh"))
+    stale = not os.path.exists(EMU_LIB) or any(os.path.getmtime(EMU_LIB) < os.path.getmtime(p)
+                                                for p in [EMU_SRC, *hdrs])
+    if stale:
+        os.makedirs(os.path.dirname(EMU_LIB), exist_ok=True)
+        subprocess.run(["/usr/local/cuda/bin/nvcc", "-O2", "-std=c++17", "-gencode",
+                        "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC", "-shared", "-o", EMU_LIB, EMU_SRC],
+                       check=True, capture_output=True)
+    return EMU_LIB
+
+
+def load_emu(path=EMU_LIB):
+    import ctypes as C
+    lib = C.CDLL(path)
+    f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+    u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+    lib.emu_stage1.argtypes = [f32p, C.c_uint64, C.c_uint64, C.c_uint32, u32p, C.c_uint32, C.c_int, C.c_uint64,
+                               f32p, u32p, C.POINTER(C.c_uint32)]
+    lib.emu_stage1.restype = C.c_int
+    lib.emu_slice_summary.argtypes = [f32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, u32p,
+                                      C.POINTER(C.c_uint32)]
+    lib.emu_slice_summary.restype = C.c_int
+    lib.emu_merge_summaries.argtypes = [u32p, C.c_uint32, C.c_uint64, C.c_uint32, f32p, u32p]
+    lib.emu_merge_summaries.restype = C.c_int
+    return lib
+
+
+@pytest.fixture(scope="session")
+def emu():
+    return load_emu(build_emu())

@@ -248,3 +248,29 @@ def test_c3_full_size_vs_reference(cuda, ref):
     rv, ri = ref.approx_top_k_batch(f, 128, 4, 287)
     assert np.array_equal(bits(v), bits(rv)) and np.array_equal(u32(i), ri)
     _invariants(f, v, i, 287)
+
+
+def test_sharded_topk_nccl_single_rank(cuda, stage_fixtures):
+    """shard.ShardedTopK through a real NCCL group (world 1 on one GPU):
+    summary -> all_gather_into_tensor -> merge == the reference result."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2506_04165_b200.shard import ShardedTopK
+    spec = INPUTS["c5_mini"]
+    x = to_device(spec, cuda).reshape(-1)
+    p = params(spec)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    store = dist.TCPStore("127.0.0.1", port, 1, True)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=cuda)
+    try:
+        v, i = ShardedTopK(p)(x)
+        torch.cuda.synchronize()
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(bits(v), bits(stage_fixtures["c5_mini/approx_v"][0]))
+    assert np.array_equal(u32(i), stage_fixtures["c5_mini/approx_i"][0])

@@ -13,30 +13,6 @@ import subprocess
 import numpy as np
 import pytest
 
-from tests.conftest import ROOT
-
-EMU_SRC = os.path.join(ROOT, "tests", "emu", "summary_emu.cu")
-EMU_LIB = os.path.join(ROOT, "build", "libatkg_emu.so")
-HDRS = [os.path.join(ROOT, "paper_2506_04165_b200", "csrc", h) for h in ("stage1.cuh", "common.cuh")]
-
-
-@pytest.fixture(scope="module")
-def emu():
-    stale = not os.path.exists(EMU_LIB) or any(os.path.getmtime(EMU_LIB) < os.path.getmtime(p)
-                                                for p in [EMU_SRC, *HDRS])
-    if stale:
-        os.makedirs(os.path.dirname(EMU_LIB), exist_ok=True)
-        subprocess.run(["/usr/local/cuda/bin/nvcc", "-O2", "-std=c++17", "-gencode",
-                        "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC", "-shared", "-o", EMU_LIB, EMU_SRC],
-                       check=True, capture_output=True)
-    lib = C.CDLL(EMU_LIB)
-    f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
-    u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
-    lib.emu_stage1.argtypes = [f32p, C.c_uint64, C.c_uint64, C.c_uint32, u32p, C.c_uint32, C.c_int, C.c_uint64,
-                               f32p, u32p, C.POINTER(C.c_uint32)]
-    lib.emu_stage1.restype = C.c_int
-    return lib
-
 
 def run_emu(emu, row, B, kp, bounds, mode, seed):
     n = row.size
