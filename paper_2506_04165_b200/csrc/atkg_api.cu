@@ -356,12 +356,14 @@ RowPlan plan_rowres(int dtype, const void* in, uint64_t n, uint64_t B, uint32_t 
   const uint64_t W = B / E;
   rp.TPR = static_cast<uint32_t>(std::min<uint64_t>(256, (W + 31) / 32 * 32));
   const size_t key_bytes = esz == 2 ? 4 : 8;  // bf16 rows use 32-bit rank keys
-  // keys (+ k more as the select scratch for large P) | pass-2 logs (also the
-  // select histogram)
-  const size_t keys = (size_t)(rp.P + (rp.P > 512 ? rp.P : 0)) * key_bytes;  // (P > 512: select scratch)
-  const size_t logs = std::max<size_t>((size_t)E * row_slots_max(kp) * rp.TPR * 4, 264 * 4);
-  const size_t per_row = ((row_bytes + 127) & ~127ull) + keys + logs;
-  rp.R = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(256 / rp.TPR, (96 * 1024) / per_row)));
+  // keys (+ P more as the select scratch for large P) | select histogram
+  const size_t keys = (size_t)(rp.P + (rp.P > 512 ? rp.P : 0)) * key_bytes;
+  const size_t scratch = 264 * 4;
+  const size_t per_row = ((row_bytes + 127) & ~127ull) + keys + scratch;
+  // small CTAs (one row when rows are large) keep many rows in flight per SM
+  const uint64_t rmax = env_u64("ATKG_ROWRES_R", 0);
+  rp.R = static_cast<uint32_t>(
+      rmax ? rmax : std::max<uint64_t>(1, std::min<uint64_t>(128 / rp.TPR, (48 * 1024) / per_row)));
   rp.smem = rp.R * per_row;
   rp.ok = true;
   return rp;

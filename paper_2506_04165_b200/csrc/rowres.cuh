@@ -9,13 +9,17 @@
 //           adjacent buckets) and runs a branch-free min/max sorting network
 //           over its stride-rows (packed bf16x2 ops for bf16) -> each
 //           bucket's exact K'-th largest value v*;
-//   pass 2  the same thread pushes only elements >= v* through the exact
-//           summary update (stage1.cuh Summ::push).  By the S* lemma, Alg. 1
+//   pass 2  the same thread marks the elements >= v* in per-bucket bit
+//           masks (one packed compare per word, a predicated OR per
+//           element), then pushes only the marked elements, in position
+//           order, through the exact summary update (summ.cuh
+//           Summ::push).  By the S* lemma, Alg. 1
 //           over the subsequence {x >= v*} ends in the same state as over
 //           the whole bucket (/root/reference/proj/core/src/topk.cpp:80-102),
 //           so finalize() yields the reference grid bit-for-bit;
 //   stage 2 the row's candidate rank keys (value desc, index asc) are
-//           bitonic-sorted in shared memory and the top K emitted.
+//           sorted (warp register bitonic sorts; two warps each sort half
+//           and a merge-path pass emits the first K) and the top K emitted.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -193,12 +197,32 @@ struct WordNet<float> {
 };
 
 // CTA = R row groups of TPR threads (TPR a multiple of 32).
-// smem: R rows of n elements | R x P candidate keys | R x E x LOGC x TPR
-// pass-2 position logs.
-// positions logged per (thread, bucket) in pass 2: K' plus room for ties
-template <int KP>
-constexpr int row_log_cap() { return KP + 6; }
-constexpr int row_slots_max(int kp) { return kp + 7; }  // + a dump slot the cursor saturates on
+// smem: R rows of n elements | R x key_stride candidate keys | R x 264 words
+// of select scratch (P > 512 only)
+constexpr uint32_t kRowMaskChunks = 8;  // stride-rows marked per sweep: 8 x 32
+constexpr int kRowFastChunks = 4;       // closed-form pass 2 for buckets of <= 128
+
+// first k of the merge of two ascending runs a[0..na), b[0..nb) of unique keys
+// (merge path: thread t emits outputs [d0, d1))
+template <typename K, typename Emit>
+__device__ __forceinline__ void merge_path_emit(const K* a, uint32_t na, const K* b, uint32_t nb, uint32_t k,
+                                                uint32_t t, uint32_t nt, Emit&& emit) {
+  const uint32_t per = (k + nt - 1) / nt;
+  const uint32_t d0 = t * per, d1 = min(k, d0 + per);
+  if (d0 >= d1) return;
+  // i + j = d0 with a[i-1] < b[j] and b[j-1] < a[i]
+  uint32_t lo = d0 > nb ? d0 - nb : 0, hi = min(d0, na);
+  while (lo < hi) {
+    const uint32_t i = (lo + hi) / 2, j = d0 - i;
+    if (a[i] < b[j - 1]) lo = i + 1;
+    else hi = i;
+  }
+  uint32_t i = lo, j = d0 - lo;
+  for (uint32_t d = d0; d < d1; ++d) {
+    const bool take_a = j >= nb || (i < na && a[i] < b[j]);
+    emit(d, take_a ? a[i++] : b[j++]);
+  }
+}
 
 template <typename T, int KP>
 __global__ void __launch_bounds__(256)
@@ -220,7 +244,7 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
   const uint32_t row_stride_b = (row_bytes + 127) & ~127u;
   const uint32_t key_stride = P > 512u ? 2 * P : P;  // + select scratch
   Key* keys = reinterpret_cast<Key*>(smem_raw + (size_t)R * row_stride_b);
-  uint32_t* logs = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(keys) + (size_t)R * key_stride * sizeof(Key));
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(keys) + (size_t)R * key_stride * sizeof(Key));
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar, 1);
     ptx::fence_mbar_init();
@@ -239,70 +263,56 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
   const uint32_t W = B / E;      // words per stride-row
   const uint32_t nstr = n / B;   // stride-rows
   Key* rkeys = keys + (uint64_t)g * key_stride;
-  constexpr int kRowLog = row_log_cap<KP>();
-  constexpr int kRowSlots = kRowLog + 1;
-  const uint32_t log_stride = E * kRowSlots * TPR > 264u ? E * kRowSlots * TPR : 264u;
-  uint32_t* mylog = logs + (uint64_t)g * log_stride + t;  // [e][slot][TPR]
   uint32_t nan = 0;
   for (uint32_t p = t; row_ok && p < W; p += TPR) {
     // pass 1: exact K'-th largest values of the E buckets of word column p
     uint32_t net[KP];
     Net::template init<KP>(net);
+#ifdef ATKG_RR_ILP2
+    {  // two independent chains (even / odd stride-rows), merged at the end
+      uint32_t net2[KP];
+      Net::template init<KP>(net2);
+      uint32_t j = 0;
+      for (; j + 1 < nstr; j += 2) {
+        Net::template add<KP>(net, words[j * W + p]);
+        Net::template add<KP>(net2, words[(j + 1) * W + p]);
+      }
+      if (j < nstr) Net::template add<KP>(net, words[j * W + p]);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) Net::template add<KP>(net, net2[k]);
+    }
+#else
     for (uint32_t j = 0; j < nstr; ++j) Net::template add<KP>(net, words[j * W + p]);
-    float vstar[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) vstar[e] = Net::lane(net[KP - 1], e);
-    // pass 2a: log the stride-rows of the elements >= v* (branch-free)
-    uint32_t cnt[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) cnt[e] = 0;
+#endif
     const uint32_t vs = net[KP - 1];  // packed v* of the word's buckets
-    // per-bucket log cursors (bytes); they saturate at slot kRowLog, which
-    // marks an overflow (heavy ties) and sends the bucket to the full replay
-    uint32_t lp[E], lend[E];
-    const uint32_t lbase = (uint32_t)__cvta_generic_to_shared(mylog);
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      lp[e] = lbase + e * kRowSlots * TPR * 4;
-      lend[e] = lp[e] + kRowLog * TPR * 4;  // the dump slot
-    }
-    const uint32_t lstride = TPR * 4;
-    for (uint32_t j = 0; j < nstr; ++j) {
-      bool h[E];
-      Net::hit(words[j * W + p], vs, h);
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        if (h[e]) {
-          asm volatile("st.shared.u32 [%0], %1;" ::"r"(lp[e]), "r"(j) : "memory");
-          lp[e] += lstride;
-        }
-        lp[e] = lp[e] < lend[e] ? lp[e] : lend[e];
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < E; ++e) cnt[e] = (lp[e] - (lbase + e * kRowSlots * TPR * 4)) / lstride;
-    // pass 2b: exact summaries of the logged elements (S* = {x >= v*});
-    // a bucket with kRowLog or more such elements (heavy ties) replays
-    // its whole stride-row sequence instead
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      Summ<KP> s;
-      s.clear();
-      const uint32_t b = p * E + e;
-      if (cnt[e] < (uint32_t)kRowLog) {
-        for (uint32_t q = 0; q < cnt[e]; ++q) {
-          const uint32_t j = mylog[(e * kRowSlots + q) * TPR];
-          s.push(Net::lane(words[j * W + p], e), j * B + b, nan);
-        }
-      } else {
-        for (uint32_t j = 0; j < nstr; ++j) {
-          const float x = Net::lane(words[j * W + p], e);
-          if (!(x < vstar[e])) s.push(x, j * B + b, nan);
-        }
-      }
+#ifdef ATKG_RR_NOPASS2
+    {
       float ov[KP];
       uint32_t oi[KP];
-      s.finalize(ov, oi);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+#pragma unroll
+        for (int kk = 0; kk < KP; ++kk) { ov[kk] = Net::lane(net[kk], e); oi[kk] = kk * B + p * E + e; }
+#pragma unroll
+        for (int kk = 0; kk < KP; ++kk) {
+          if (grid_v) {
+            grid_v[row * KP * B + (uint64_t)kk * B + p * E + e] = ov[kk];
+            grid_i[row * KP * B + (uint64_t)kk * B + p * E + e] = oi[kk];
+          }
+          if ((uint32_t)kk < filled) {
+            if constexpr (K32) rkeys[(uint64_t)kk * B + p * E + e] = rank_key32_bf16(__float_as_uint(ov[kk]), oi[kk]);
+            else rkeys[(uint64_t)kk * B + p * E + e] = rank_key_bits(__float_as_uint(ov[kk]), oi[kk]);
+          }
+        }
+      }
+      continue;
+    }
+#endif
+    Summ<KP> s[E];
+    bool done[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { s[e].clear(); done[e] = false; }
+    auto store = [&](uint32_t b, const float (&ov)[KP], const uint32_t (&oi)[KP]) {
 #pragma unroll
       for (int kk = 0; kk < KP; ++kk) {
         if (grid_v) {
@@ -314,6 +324,140 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
           else rkeys[(uint64_t)kk * B + b] = rank_key_bits(__float_as_uint(ov[kk]), oi[kk]);
         }
       }
+    };
+    // pass 2: sweeps of up to 256 stride-rows: mark the elements >= v*
+    // (NaN included) in bit masks, then push the marked ones in order
+    for (uint32_t j0 = 0; j0 < nstr; j0 += 32 * kRowMaskChunks) {
+      uint32_t mk[E][kRowMaskChunks];
+#pragma unroll
+      for (int c = 0; c < (int)kRowMaskChunks; ++c) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) mk[e][c] = 0;
+        const uint32_t jc = j0 + 32 * c;
+        if (jc + 32 <= nstr) {
+          const uint32_t* wp = words + jc * W + p;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            bool h[E];
+            Net::hit(wp[q * W], vs, h);
+#pragma unroll
+            for (int e = 0; e < E; ++e) mk[e][c] |= h[e] ? (1u << q) : 0u;
+          }
+        } else if (jc < nstr) {
+          for (uint32_t q = 0; q < nstr - jc; ++q) {
+            bool h[E];
+            Net::hit(words[(jc + q) * W + p], vs, h);
+#pragma unroll
+            for (int e = 0; e < E; ++e) mk[e][c] |= h[e] ? (1u << q) : 0u;
+          }
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t b = p * E + e;
+        if (nstr <= 32 * kRowFastChunks && Net::lane(vs, e) > neg_inf()) {
+          // closed form of Alg. 1 over S* = {x >= v*} (summ.cuh finalize):
+          // keep every big (x > v*), the first c-1 ties (x == v*, c = K' -
+          // #bigs) and X = the last tie if it comes after the last big, else
+          // the c-th tie.  One pass over the marked elements, no list
+          // updates.
+          const float vst = Net::lane(vs, e);
+          uint32_t cnt = 0;
+#pragma unroll
+          for (int c = 0; c < kRowFastChunks; ++c) cnt += __popc(mk[e][c]);
+          float bv[KP];
+          uint32_t bp[KP], tp[KP];
+#pragma unroll
+          for (int kk = 0; kk < KP; ++kk) { bv[kk] = neg_inf(); bp[kk] = kEmptyPos; tp[kk] = 0; }
+          uint32_t nb = 0, nt = 0, last_big = 0, last_tie = 0;
+          for (uint32_t h = 0; h < cnt; ++h) {
+            uint32_t j = 0;
+            bool found = false;
+#pragma unroll
+            for (int c = 0; c < kRowFastChunks; ++c) {
+              if (!found && mk[e][c]) {
+                j = 32 * c + (__ffs(mk[e][c]) - 1);
+                mk[e][c] &= mk[e][c] - 1;
+                found = true;
+              }
+            }
+            const float x = Net::lane(words[j * W + p], e);
+            const uint32_t pos = j * B + b;
+            if (x != x) {
+              nan = 1u;
+            } else if (x > vst) {
+#pragma unroll
+              for (int kk = 0; kk < KP - 1; ++kk)
+                if ((uint32_t)kk == nb) { bv[kk] = x; bp[kk] = pos; }
+              ++nb;
+              last_big = pos;
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < KP; ++kk)
+                if ((uint32_t)kk == nt) tp[kk] = pos;
+              ++nt;
+              last_tie = pos;
+            }
+          }
+          // bigs: stable sort by value desc (empty slots are -inf, sink)
+#pragma unroll
+          for (int i = 1; i < KP - 1; ++i) {
+#pragma unroll
+            for (int kk = i; kk >= 1; --kk) {
+              const bool sw = bv[kk] > bv[kk - 1];
+              const float tv = bv[kk];
+              const uint32_t ti = bp[kk];
+              bv[kk] = sw ? bv[kk - 1] : tv;
+              bp[kk] = sw ? bp[kk - 1] : ti;
+              bv[kk - 1] = sw ? tv : bv[kk - 1];
+              bp[kk - 1] = sw ? ti : bp[kk - 1];
+            }
+          }
+          const uint32_t c = KP - nb;  // ties kept (>= 1)
+          uint32_t tc = 0;             // the c-th tie
+#pragma unroll
+          for (int kk = 0; kk < KP; ++kk)
+            if ((uint32_t)kk + 1 == c) tc = tp[kk];
+          const uint32_t X = (nb == 0 || last_tie > last_big) ? last_tie : tc;
+          float ov[KP];
+          uint32_t oi[KP];
+#pragma unroll
+          for (int kk = 0; kk < KP; ++kk) {
+            if ((uint32_t)kk < nb) {
+              ov[kk] = bv[kk];
+              oi[kk] = bp[kk];
+            } else {
+              const uint32_t ti = kk - nb;  // tie rank
+              uint32_t tpos = X;
+#pragma unroll
+              for (int q = 0; q < KP; ++q)
+                if ((uint32_t)q == ti && ti + 1 < c) tpos = tp[q];
+              ov[kk] = vst;
+              oi[kk] = tpos;
+            }
+          }
+          store(b, ov, oi);
+          done[e] = true;
+          continue;
+        }
+#pragma unroll
+        for (int c = 0; c < (int)kRowMaskChunks; ++c) {
+          uint32_t m = mk[e][c];
+          while (m) {
+            const uint32_t j = j0 + 32 * c + (__ffs(m) - 1);
+            m &= m - 1;
+            s[e].push(Net::lane(words[j * W + p], e), j * B + b, nan);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (done[e]) continue;
+      float ov[KP];
+      uint32_t oi[KP];
+      s[e].finalize(ov, oi);
+      store(p * E + e, ov, oi);
     }
   }
   if (nan) atomicOr(status, ATKG_FLAG_NAN);
@@ -323,9 +467,35 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
   if (P > 512u) {
     // large candidate sets: radix-select the k smallest (unique) keys into
     // the front, then sort only those
-    group_select_front<Key>(rkeys, P, k, t, TPR, logs + (uint64_t)g * log_stride);
+    group_select_front<Key>(rkeys, P, k, t, TPR, scratch + (uint64_t)g * 264);
     nsort = 2;
     while (nsort < k) nsort <<= 1;
+  }
+  auto emit = [&](uint32_t q, Key key) {
+    if constexpr (K32) {
+      out_v[row * k + q] = key32_value_bf16(key);
+      out_i[row * k + q] = key & 0xffffu;
+    } else {
+      out_v[row * k + q] = __uint_as_float(key_value_bits(key));
+      out_i[row * k + q] = (uint32_t)key;
+    }
+  };
+  if (nsort == 512u && TPR >= 64) {
+    // two warps each sort 256 keys in registers; merge path emits the first k
+    if (row_ok && t < 64) {
+      Key kk[8];
+      Key* half = rkeys + (t / 32) * 256;
+      const uint32_t l = t % 32;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) kk[r] = half[l * 8 + r];
+      warp_bitonic_sort<Key, 8>(kk, (int)l);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) half[l * 8 + r] = kk[r];
+    }
+    __syncthreads();
+    if (!row_ok || (*status & ATKG_FLAG_NAN)) return;
+    merge_path_emit<Key>(rkeys, 256, rkeys + 256, 256, k, t, TPR, emit);
+    return;
   }
   if (nsort == 512u || nsort == 256u) {
     // one warp of the row group sorts in registers
@@ -351,15 +521,7 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
     group_bitonic_sort<Key>(rkeys, nsort, t, TPR);
   }
   if (!row_ok || (*status & ATKG_FLAG_NAN)) return;
-  for (uint32_t q = t; q < k; q += TPR) {
-    if constexpr (K32) {
-      out_v[row * k + q] = key32_value_bf16(rkeys[q]);
-      out_i[row * k + q] = rkeys[q] & 0xffffu;
-    } else {
-      out_v[row * k + q] = __uint_as_float(key_value_bits(rkeys[q]));
-      out_i[row * k + q] = (uint32_t)rkeys[q];
-    }
-  }
+  for (uint32_t q = t; q < k; q += TPR) emit(q, rkeys[q]);
 }
 
 }  // namespace atkg

@@ -274,3 +274,29 @@ def test_sharded_topk_nccl_single_rank(cuda, stage_fixtures):
         dist.destroy_process_group()
     assert np.array_equal(bits(v), bits(stage_fixtures["c5_mini/approx_v"][0]))
     assert np.array_equal(u32(i), stage_fixtures["c5_mini/approx_i"][0])
+
+
+@pytest.mark.parametrize("levels,B,kp,k", [(7, 128, 4, 287), (40, 128, 4, 287), (3, 256, 4, 100), (25, 128, 8, 300),
+                                           (12, 512, 2, 200), (5, 3584, 1, 287)])
+def test_rowres_ties_vs_reference(cuda, ref, levels, B, kp, k):
+    """Row-resident path (bf16 rows of 14336) on heavily tied data: the
+    closed-form pass 2 (bigs, first c-1 ties, last-tie rule) and the K'-th
+    value ties must reproduce the reference bit for bit."""
+    rng = np.random.default_rng(levels * 1000 + B)
+    rows = 64
+    q = rng.integers(-levels, levels + 1, size=(rows, 14336)).astype(np.float32) / 4.0
+    q[3, ::7] = -np.inf
+    q[5] = 0.0
+    q[6, 100:200] = -0.0
+    from paper_2506_04165_b200 import data
+    bits16 = data.f32_to_bf16_bits(q)
+    f = data.bf16_bits_to_f32(bits16)
+    xb = torch.from_numpy(bits16.view(np.int16)).to(cuda).view(torch.bfloat16)
+    p = atk.AlgoParams(14336, B, kp, k)
+    v, i = atk.approx_top_k_device(xb, p)
+    rv, ri = ref.approx_top_k_batch(f, B, kp, k)
+    assert np.array_equal(bits(v), bits(rv)) and np.array_equal(u32(i), ri)
+    gv, gi = atk.stage1_device(xb, p)
+    rg = [ref.stage1(f[r], B, kp) for r in range(4)]
+    for r in range(4):
+        assert np.array_equal(bits(gv[r]), bits(rg[r][0])) and np.array_equal(u32(gi[r]), rg[r][1])
