@@ -199,7 +199,6 @@ struct WordNet<float> {
 // CTA = R row groups of TPR threads (TPR a multiple of 32).
 // smem: R rows of n elements | R x key_stride candidate keys | R x 264 words
 // of select scratch (P > 512 only)
-constexpr uint32_t kRowMaskChunks = 8;  // stride-rows marked per sweep: 8 x 32
 constexpr int kRowFastChunks = 4;       // closed-form pass 2 for buckets of <= 128
 
 // first k of the merge of two ascending runs a[0..na), b[0..nb) of unique keys
@@ -308,10 +307,6 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
       continue;
     }
 #endif
-    Summ<KP> s[E];
-    bool done[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) { s[e].clear(); done[e] = false; }
     auto store = [&](uint32_t b, const float (&ov)[KP], const uint32_t (&oi)[KP]) {
 #pragma unroll
       for (int kk = 0; kk < KP; ++kk) {
@@ -325,139 +320,156 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
         }
       }
     };
-    // pass 2: sweeps of up to 256 stride-rows: mark the elements >= v*
-    // (NaN included) in bit masks, then push the marked ones in order
-    for (uint32_t j0 = 0; j0 < nstr; j0 += 32 * kRowMaskChunks) {
-      uint32_t mk[E][kRowMaskChunks];
+    uint32_t done = 0;  // buckets of this word finished by the closed form
+    if (nstr <= 32 * kRowFastChunks) {
+      // pass 2: mark the elements >= v* (NaN included) in per-bucket bit
+      // masks: one packed compare per word, a predicated OR per element
+      uint32_t mk[E][kRowFastChunks];
+      uint32_t base[kRowFastChunks];  // first stride-row of each chunk's window
+      if (nstr >= 32) {
+        // full 32-row windows; the last one is shifted back to end at nstr
+        // and its rows already covered by the previous chunk are masked off
 #pragma unroll
-      for (int c = 0; c < (int)kRowMaskChunks; ++c) {
+        for (int c = 0; c < kRowFastChunks; ++c) {
+          const uint32_t jc = 32 * c;
+          base[c] = min(jc, nstr - 32);
 #pragma unroll
-        for (int e = 0; e < E; ++e) mk[e][c] = 0;
-        const uint32_t jc = j0 + 32 * c;
-        if (jc + 32 <= nstr) {
-          const uint32_t* wp = words + jc * W + p;
+          for (int e = 0; e < E; ++e) mk[e][c] = 0;
+          if (jc < nstr) {
+            const uint32_t* wp = words + base[c] * W + p;
 #pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            bool h[E];
-            Net::hit(wp[q * W], vs, h);
+            for (int q = 0; q < 32; ++q) {
+              bool h[E];
+              Net::hit(wp[q * W], vs, h);
 #pragma unroll
-            for (int e = 0; e < E; ++e) mk[e][c] |= h[e] ? (1u << q) : 0u;
+              for (int e = 0; e < E; ++e) mk[e][c] |= h[e] ? (1u << q) : 0u;
+            }
+            const uint32_t skip = jc - base[c];  // rows owned by the previous chunk
+#pragma unroll
+            for (int e = 0; e < E; ++e) mk[e][c] &= ~((1u << skip) - 1u);
           }
-        } else if (jc < nstr) {
-          for (uint32_t q = 0; q < nstr - jc; ++q) {
-            bool h[E];
-            Net::hit(words[(jc + q) * W + p], vs, h);
+        }
+      } else {
 #pragma unroll
-            for (int e = 0; e < E; ++e) mk[e][c] |= h[e] ? (1u << q) : 0u;
+        for (int c = 0; c < kRowFastChunks; ++c) {
+          base[c] = 0;
+#pragma unroll
+          for (int e = 0; e < E; ++e) mk[e][c] = 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          if ((uint32_t)q < nstr) {
+            bool h[E];
+            Net::hit(words[q * W + p], vs, h);
+#pragma unroll
+            for (int e = 0; e < E; ++e) mk[e][0] |= h[e] ? (1u << q) : 0u;
           }
         }
       }
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const uint32_t b = p * E + e;
-        if (nstr <= 32 * kRowFastChunks && Net::lane(vs, e) > neg_inf()) {
-          // closed form of Alg. 1 over S* = {x >= v*} (summ.cuh finalize):
-          // keep every big (x > v*), the first c-1 ties (x == v*, c = K' -
-          // #bigs) and X = the last tie if it comes after the last big, else
-          // the c-th tie.  One pass over the marked elements, no list
-          // updates.
-          const float vst = Net::lane(vs, e);
-          uint32_t cnt = 0;
+        const float vst = Net::lane(vs, e);
+        if (!(vst > neg_inf())) continue;  // v* = -inf: sentinel rules, general path
+        // closed form of Alg. 1 over S* = {x >= v*} (summ.cuh finalize):
+        // keep every big (x > v*), the first c-1 ties (x == v*, c = K' -
+        // #bigs) and X = the last tie if it comes after the last big, else
+        // the c-th tie.  One pass over the marked elements, no list updates.
+        uint32_t cnt = 0;
 #pragma unroll
-          for (int c = 0; c < kRowFastChunks; ++c) cnt += __popc(mk[e][c]);
-          float bv[KP];
-          uint32_t bp[KP], tp[KP];
+        for (int c = 0; c < kRowFastChunks; ++c) cnt += __popc(mk[e][c]);
+        float bv[KP];
+        uint32_t bp[KP], tp[KP];
 #pragma unroll
-          for (int kk = 0; kk < KP; ++kk) { bv[kk] = neg_inf(); bp[kk] = kEmptyPos; tp[kk] = 0; }
-          uint32_t nb = 0, nt = 0, last_big = 0, last_tie = 0;
-          for (uint32_t h = 0; h < cnt; ++h) {
-            uint32_t j = 0;
-            bool found = false;
+        for (int kk = 0; kk < KP; ++kk) { bv[kk] = neg_inf(); bp[kk] = kEmptyPos; tp[kk] = 0; }
+        uint32_t nb = 0, nt = 0, last_big = 0, last_tie = 0;
+        for (uint32_t h = 0; h < cnt; ++h) {
+          uint32_t j = 0;
+          bool found = false;
 #pragma unroll
-            for (int c = 0; c < kRowFastChunks; ++c) {
-              if (!found && mk[e][c]) {
-                j = 32 * c + (__ffs(mk[e][c]) - 1);
-                mk[e][c] &= mk[e][c] - 1;
-                found = true;
-              }
-            }
-            const float x = Net::lane(words[j * W + p], e);
-            const uint32_t pos = j * B + b;
-            if (x != x) {
-              nan = 1u;
-            } else if (x > vst) {
-#pragma unroll
-              for (int kk = 0; kk < KP - 1; ++kk)
-                if ((uint32_t)kk == nb) { bv[kk] = x; bp[kk] = pos; }
-              ++nb;
-              last_big = pos;
-            } else {
-#pragma unroll
-              for (int kk = 0; kk < KP; ++kk)
-                if ((uint32_t)kk == nt) tp[kk] = pos;
-              ++nt;
-              last_tie = pos;
+          for (int c = 0; c < kRowFastChunks; ++c) {
+            if (!found && mk[e][c]) {
+              j = base[c] + (__ffs(mk[e][c]) - 1);
+              mk[e][c] &= mk[e][c] - 1;
+              found = true;
             }
           }
-          // bigs: stable sort by value desc (empty slots are -inf, sink)
+          const float x = Net::lane(words[j * W + p], e);
+          const uint32_t pos = j * B + b;
+          if (x != x) {
+            nan = 1u;
+          } else if (x > vst) {
 #pragma unroll
-          for (int i = 1; i < KP - 1; ++i) {
+            for (int kk = 0; kk < KP - 1; ++kk)
+              if ((uint32_t)kk == nb) { bv[kk] = x; bp[kk] = pos; }
+            ++nb;
+            last_big = pos;
+          } else {
 #pragma unroll
-            for (int kk = i; kk >= 1; --kk) {
-              const bool sw = bv[kk] > bv[kk - 1];
-              const float tv = bv[kk];
-              const uint32_t ti = bp[kk];
-              bv[kk] = sw ? bv[kk - 1] : tv;
-              bp[kk] = sw ? bp[kk - 1] : ti;
-              bv[kk - 1] = sw ? tv : bv[kk - 1];
-              bp[kk - 1] = sw ? ti : bp[kk - 1];
-            }
-          }
-          const uint32_t c = KP - nb;  // ties kept (>= 1)
-          uint32_t tc = 0;             // the c-th tie
-#pragma unroll
-          for (int kk = 0; kk < KP; ++kk)
-            if ((uint32_t)kk + 1 == c) tc = tp[kk];
-          const uint32_t X = (nb == 0 || last_tie > last_big) ? last_tie : tc;
-          float ov[KP];
-          uint32_t oi[KP];
-#pragma unroll
-          for (int kk = 0; kk < KP; ++kk) {
-            if ((uint32_t)kk < nb) {
-              ov[kk] = bv[kk];
-              oi[kk] = bp[kk];
-            } else {
-              const uint32_t ti = kk - nb;  // tie rank
-              uint32_t tpos = X;
-#pragma unroll
-              for (int q = 0; q < KP; ++q)
-                if ((uint32_t)q == ti && ti + 1 < c) tpos = tp[q];
-              ov[kk] = vst;
-              oi[kk] = tpos;
-            }
-          }
-          store(b, ov, oi);
-          done[e] = true;
-          continue;
-        }
-#pragma unroll
-        for (int c = 0; c < (int)kRowMaskChunks; ++c) {
-          uint32_t m = mk[e][c];
-          while (m) {
-            const uint32_t j = j0 + 32 * c + (__ffs(m) - 1);
-            m &= m - 1;
-            s[e].push(Net::lane(words[j * W + p], e), j * B + b, nan);
+            for (int kk = 0; kk < KP; ++kk)
+              if ((uint32_t)kk == nt) tp[kk] = pos;
+            ++nt;
+            last_tie = pos;
           }
         }
+        // bigs: stable sort by value desc (empty slots are -inf and sink)
+#pragma unroll
+        for (int i = 1; i < KP - 1; ++i) {
+#pragma unroll
+          for (int kk = i; kk >= 1; --kk) {
+            const bool sw = bv[kk] > bv[kk - 1];
+            const float tv = bv[kk];
+            const uint32_t ti = bp[kk];
+            bv[kk] = sw ? bv[kk - 1] : tv;
+            bp[kk] = sw ? bp[kk - 1] : ti;
+            bv[kk - 1] = sw ? tv : bv[kk - 1];
+            bp[kk - 1] = sw ? ti : bp[kk - 1];
+          }
+        }
+        const uint32_t c = KP - nb;  // ties kept (>= 1)
+        uint32_t tc = 0;             // the c-th tie
+#pragma unroll
+        for (int kk = 0; kk < KP; ++kk)
+          if ((uint32_t)kk + 1 == c) tc = tp[kk];
+        const uint32_t X = (nb == 0 || last_tie > last_big) ? last_tie : tc;
+        float ov[KP];
+        uint32_t oi[KP];
+#pragma unroll
+        for (int kk = 0; kk < KP; ++kk) {
+          if ((uint32_t)kk < nb) {
+            ov[kk] = bv[kk];
+            oi[kk] = bp[kk];
+          } else {
+            const uint32_t ti = kk - nb;  // tie rank
+            uint32_t tpos = X;
+#pragma unroll
+            for (int q = 0; q < KP; ++q)
+              if ((uint32_t)q == ti && ti + 1 < c) tpos = tp[q];
+            ov[kk] = vst;
+            oi[kk] = tpos;
+          }
+        }
+        store(b, ov, oi);
+        done |= 1u << e;
       }
     }
-#pragma unroll
+    // general path (long buckets, v* = -inf): exact summary update over the
+    // elements >= v* in position order
+#pragma unroll 1
     for (int e = 0; e < E; ++e) {
-      if (done[e]) continue;
+      if (done >> e & 1u) continue;
+      const uint32_t b = p * E + e;
+      const float vst = Net::lane(vs, e);
+      Summ<KP> sm;
+      sm.clear();
+      for (uint32_t j = 0; j < nstr; ++j) {
+        const float x = Net::lane(words[j * W + p], e);
+        if (!(x < vst)) sm.push(x, j * B + b, nan);
+      }
       float ov[KP];
       uint32_t oi[KP];
-      s[e].finalize(ov, oi);
-      store(p * E + e, ov, oi);
+      sm.finalize(ov, oi);
+      store(b, ov, oi);
     }
   }
   if (nan) atomicOr(status, ATKG_FLAG_NAN);
