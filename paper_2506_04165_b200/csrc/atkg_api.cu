@@ -341,6 +341,7 @@ void run_merge(const S1Plan& pl, uint32_t kp, const uint32_t* ws, uint64_t rows,
 struct RowPlan {
   bool ok = false;
   uint32_t R = 1, TPR = 32, P = 2;
+  uint32_t fast = 0;  // closed-form pass 2 (short buckets, window padding affordable)
   size_t smem = 0;
 };
 RowPlan plan_rowres(int dtype, const void* in, uint64_t n, uint64_t B, uint32_t kp) {
@@ -364,7 +365,14 @@ RowPlan plan_rowres(int dtype, const void* in, uint64_t n, uint64_t B, uint32_t 
   const uint64_t rmax = env_u64("ATKG_ROWRES_R", 0);
   rp.R = static_cast<uint32_t>(
       rmax ? rmax : std::max<uint64_t>(1, std::min<uint64_t>(128 / rp.TPR, (48 * 1024) / per_row)));
-  rp.smem = rp.R * per_row;
+  // pass 2 reads whole 32/E-row windows: rows past the end land in the
+  // bytes that follow the last row (keys, scratch, then padding)
+  const uint64_t CH = 32 / E, nstr = n / B;
+  const size_t over = (size_t)((CH - nstr % CH) % CH) * B * esz;  // window overrun past the row
+  const size_t tail = rp.R * (keys + scratch);
+  const size_t pad = over > tail ? over - tail : 0;
+  rp.fast = (nstr <= 128 && pad <= 4096 && !env_u64("ATKG_RR_SLOW", 0)) ? 1u : 0u;
+  rp.smem = rp.R * per_row + (rp.fast ? pad : 0);
   rp.ok = true;
   return rp;
 }
@@ -380,7 +388,8 @@ void launch_rowres(const RowPlan& rp, const void* in, uint64_t rows, uint64_t n,
   const uint32_t filled = (uint32_t)std::min<uint64_t>(KP, n / B);
   g_prof.bracket_begin(st);
   kern<<<static_cast<unsigned>(ceil_div(rows, rp.R)), rp.R * rp.TPR, rp.smem, st>>>(
-      static_cast<const T*>(in), rows, (uint32_t)n, (uint32_t)B, rp.R, k, filled, rp.P, ov, oi, gv, gi, status);
+      static_cast<const T*>(in), rows, (uint32_t)n, (uint32_t)B, rp.R, k, filled, rp.P, rp.fast, ov, oi, gv, gi,
+      status);
   check_launch();
   g_prof.bracket_end(st);
 }

@@ -157,6 +157,12 @@ struct WordNet<__nv_bfloat16> {
   __device__ __forceinline__ static float lane(uint32_t w, int e) {
     return __uint_as_float(e ? (w & 0xffff0000u) : (w << 16));
   }
+  // per-half !(x < v*) (NaN included) as 0xffff / 0 halves (one HSET2)
+  __device__ __forceinline__ static uint32_t hitmask(uint32_t w, uint32_t vs) {
+    uint32_t r;
+    asm("set.geu.u32.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(w), "r"(vs));
+    return r;
+  }
   // per-half !(x < v*) (NaN included) as two predicates from one HSETP2
   __device__ __forceinline__ static void hit(uint32_t w, uint32_t vs, bool (&h)[2]) {
     uint32_t lo, hi;
@@ -191,6 +197,11 @@ struct WordNet<float> {
     }
   }
   __device__ __forceinline__ static float lane(uint32_t w, int) { return __uint_as_float(w); }
+  __device__ __forceinline__ static uint32_t hitmask(uint32_t w, uint32_t vs) {
+    uint32_t r;
+    asm("set.geu.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(w)), "f"(__uint_as_float(vs)));
+    return r;
+  }
   __device__ __forceinline__ static void hit(uint32_t w, uint32_t vs, bool (&h)[1]) {
     h[0] = !(__uint_as_float(w) < __uint_as_float(vs));
   }
@@ -226,7 +237,8 @@ __device__ __forceinline__ void merge_path_emit(const K* a, uint32_t na, const K
 template <typename T, int KP>
 __global__ void __launch_bounds__(256)
 row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_t B, uint32_t R, uint32_t k,
-                    uint32_t filled, uint32_t P, float* out_v, uint32_t* out_i, float* grid_v, uint32_t* grid_i,
+                    uint32_t filled, uint32_t P, uint32_t fast, float* out_v, uint32_t* out_i, float* grid_v,
+                    uint32_t* grid_i,
                     uint32_t* status) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using Net = WordNet<T>;
@@ -321,49 +333,35 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
       }
     };
     uint32_t done = 0;  // buckets of this word finished by the closed form
-    if (nstr <= 32 * kRowFastChunks) {
-      // pass 2: mark the elements >= v* (NaN included) in per-bucket bit
-      // masks: one packed compare per word, a predicated OR per element
-      uint32_t mk[E][kRowFastChunks];
-      uint32_t base[kRowFastChunks];  // first stride-row of each chunk's window
-      if (nstr >= 32) {
-        // full 32-row windows; the last one is shifted back to end at nstr
-        // and its rows already covered by the previous chunk are masked off
+    if (fast) {  // nstr <= 32 * kRowFastChunks and padded shared memory (host)
+      // pass 2: mark the elements >= v* (NaN included).  Chunk c holds
+      // CH = 32/E consecutive stride-rows 16c.. with bit q + e*CH for
+      // bucket e (one SET + one LOP3 per word).  Rows past nstr read the
+      // shared-memory padding that follows the row and are masked off.
+      constexpr int CH = 32 / E;
+      constexpr int NCH = 32 * kRowFastChunks / CH;
+      uint32_t mk[NCH];
+      auto qbits = [](int q) {
+        uint32_t m = 0;
 #pragma unroll
-        for (int c = 0; c < kRowFastChunks; ++c) {
-          const uint32_t jc = 32 * c;
-          base[c] = min(jc, nstr - 32);
+        for (int e = 0; e < E; ++e) m |= 1u << (q + e * CH);
+        return m;
+      };
 #pragma unroll
-          for (int e = 0; e < E; ++e) mk[e][c] = 0;
-          if (jc < nstr) {
-            const uint32_t* wp = words + base[c] * W + p;
+      for (int c = 0; c < NCH; ++c) {
+        const uint32_t jc = CH * c;
+        mk[c] = 0;
+        if (jc < nstr) {
+          const uint32_t* wp = words + jc * W + p;
+          uint32_t a0 = 0, a1 = 0;  // two chains for ILP
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
-              bool h[E];
-              Net::hit(wp[q * W], vs, h);
-#pragma unroll
-              for (int e = 0; e < E; ++e) mk[e][c] |= h[e] ? (1u << q) : 0u;
-            }
-            const uint32_t skip = jc - base[c];  // rows owned by the previous chunk
-#pragma unroll
-            for (int e = 0; e < E; ++e) mk[e][c] &= ~((1u << skip) - 1u);
+          for (int q = 0; q < CH; q += 2) {
+            a0 |= Net::hitmask(wp[q * W], vs) & qbits(q);
+            a1 |= Net::hitmask(wp[(q + 1) * W], vs) & qbits(q + 1);
           }
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < kRowFastChunks; ++c) {
-          base[c] = 0;
-#pragma unroll
-          for (int e = 0; e < E; ++e) mk[e][c] = 0;
-        }
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          if ((uint32_t)q < nstr) {
-            bool h[E];
-            Net::hit(words[q * W + p], vs, h);
-#pragma unroll
-            for (int e = 0; e < E; ++e) mk[e][0] |= h[e] ? (1u << q) : 0u;
-          }
+          const uint32_t rem = nstr - jc;
+          const uint32_t valid = rem >= (uint32_t)CH ? 0xffffffffu : ((1u << rem) - 1u) * qbits(0);
+          mk[c] = (a0 | a1) & valid;
         }
       }
 #pragma unroll
@@ -371,29 +369,45 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
         const uint32_t b = p * E + e;
         const float vst = Net::lane(vs, e);
         if (!(vst > neg_inf())) continue;  // v* = -inf: sentinel rules, general path
+        // this bucket's marks as 32-row masks m[k] (rows 32k..32k+31)
+        uint32_t m[kRowFastChunks];
+#pragma unroll
+        for (int k = 0; k < kRowFastChunks; ++k) {
+          if constexpr (E == 2) m[k] = __byte_perm(mk[2 * k], mk[2 * k + 1], e ? 0x7632 : 0x5410);
+          else m[k] = mk[k];
+        }
+#ifdef ATKG_RR_NOEXTRACT
+        {
+          float ov[KP];
+          uint32_t oi[KP];
+#pragma unroll
+          for (int kk = 0; kk < KP; ++kk) { ov[kk] = vst; oi[kk] = __popc(m[kk % kRowFastChunks]) + b; }
+          store(b, ov, oi);
+          done |= 1u << e;
+          continue;
+        }
+#endif
         // closed form of Alg. 1 over S* = {x >= v*} (summ.cuh finalize):
         // keep every big (x > v*), the first c-1 ties (x == v*, c = K' -
         // #bigs) and X = the last tie if it comes after the last big, else
         // the c-th tie.  One pass over the marked elements, no list updates.
         uint32_t cnt = 0;
 #pragma unroll
-        for (int c = 0; c < kRowFastChunks; ++c) cnt += __popc(mk[e][c]);
+        for (int k = 0; k < kRowFastChunks; ++k) cnt += __popc(m[k]);
         float bv[KP];
         uint32_t bp[KP], tp[KP];
 #pragma unroll
         for (int kk = 0; kk < KP; ++kk) { bv[kk] = neg_inf(); bp[kk] = kEmptyPos; tp[kk] = 0; }
         uint32_t nb = 0, nt = 0, last_big = 0, last_tie = 0;
         for (uint32_t h = 0; h < cnt; ++h) {
-          uint32_t j = 0;
-          bool found = false;
+          // lowest marked row: first nonzero mask word
+          const uint32_t w0 = m[0] ? m[0] : (m[1] ? m[1] : (m[2] ? m[2] : m[3]));
+          const uint32_t k0 = m[0] ? 0u : (m[1] ? 1u : (m[2] ? 2u : 3u));
+          const uint32_t j = 32 * k0 + (__ffs(w0) - 1);
+          const uint32_t wc = w0 & (w0 - 1);
 #pragma unroll
-          for (int c = 0; c < kRowFastChunks; ++c) {
-            if (!found && mk[e][c]) {
-              j = base[c] + (__ffs(mk[e][c]) - 1);
-              mk[e][c] &= mk[e][c] - 1;
-              found = true;
-            }
-          }
+          for (int k = 0; k < kRowFastChunks; ++k)
+            if ((uint32_t)k == k0) m[k] = wc;
           const float x = Net::lane(words[j * W + p], e);
           const uint32_t pos = j * B + b;
           if (x != x) {
