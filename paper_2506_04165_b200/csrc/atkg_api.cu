@@ -634,6 +634,8 @@ int atkg_workspace_size(int op, int dtype, uint64_t rows, const atkg_params* p, 
         const S1Plan pl = plan_stage1(dtype, aligned, rows, p->n, p->n, p->num_buckets, p->local_k);
         *bytes = stage1_ws_bytes(pl, rows, p->num_buckets, p->local_k) + grid_bytes(rows, *p) +
                  select_ws_bytes(rows, filled_count(*p), p->global_k);
+        const ThrPlan tp = plan_rowthr(dtype, aligned, p->n, p->num_buckets, p->local_k, p->global_k);
+        if (tp.ok) *bytes = std::max<size_t>(*bytes, rowthr_ws_bytes(rows, tp));
         break;
       }
       case ATKG_OP_SELECT:
@@ -698,6 +700,12 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     float* gv = reinterpret_cast<float*>(w);
     uint32_t* gi = reinterpret_cast<uint32_t*>(w + rows * gstride * 4);
     w += grid_bytes(rows, *p);
+    const ThrPlan tp = plan_rowthr(dtype, d_in, p->n, p->num_buckets, p->local_k, p->global_k);
+    if (tp.ok) {  // row-resident, row threshold: stage 1 + stage 2 in one warp per row
+      run_rowthr(dtype, tp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,
+                 s1ws, d_status, st);
+      return;
+    }
     const RowPlan rp = plan_rowres(dtype, d_in, p->n, p->num_buckets, p->local_k);
     if (rp.ok) {  // row-resident: stage 1 + stage 2 in one kernel
       run_rowres(dtype, rp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,

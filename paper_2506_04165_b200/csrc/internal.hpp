@@ -58,4 +58,15 @@ uint64_t select_ws_bytes(uint64_t rows, uint64_t count, uint32_t k);
 void run_select(const float* vals, const uint32_t* idx, uint64_t rows, uint64_t count, uint64_t stride, uint32_t k,
                 uint64_t limit, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
 
+// row-threshold approx_top_k for rows that fit in shared memory (rowthr.cu)
+struct ThrPlan {
+  bool ok = false;
+  uint32_t cap = 512, rsel = 1, region = 0;
+  size_t smem = 0;
+};
+ThrPlan plan_rowthr(int dtype, const void* in, uint64_t n, uint64_t B, uint32_t kp, uint32_t k);
+uint64_t rowthr_ws_bytes(uint64_t rows, const ThrPlan& tp);
+void run_rowthr(int dtype, const ThrPlan& tp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
+                uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
+
 }  // namespace atkg

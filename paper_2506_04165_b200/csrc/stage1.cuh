@@ -345,7 +345,7 @@ __global__ void fold_grid_kernel(float* gv, uint32_t* gi, uint64_t B, uint32_t k
   if (nan) atomicOr(status, ATKG_FLAG_NAN);
 }
 
-__global__ void grid_init_kernel(float* gv, uint32_t* gi, uint64_t count) {
+static __global__ void grid_init_kernel(float* gv, uint32_t* gi, uint64_t count) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < count) { gv[t] = neg_inf(); gi[t] = 0; }
 }

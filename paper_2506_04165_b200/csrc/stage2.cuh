@@ -34,7 +34,7 @@ __device__ __forceinline__ void block_bitonic_sort(uint64_t* s, uint32_t P) {
 }
 
 // row r candidates: vals/idx[r*stride + c], c < count
-__global__ void stage2_bitonic_kernel(const float* __restrict__ vals, const uint32_t* __restrict__ idx,
+static __global__ void stage2_bitonic_kernel(const float* __restrict__ vals, const uint32_t* __restrict__ idx,
                                       uint64_t count, uint64_t stride, uint32_t k, uint64_t index_limit,
                                       uint32_t P, float* out_v, uint32_t* out_i, uint32_t* status) {
   extern __shared__ uint64_t keys[];
