@@ -636,6 +636,8 @@ int atkg_workspace_size(int op, int dtype, uint64_t rows, const atkg_params* p, 
                  select_ws_bytes(rows, filled_count(*p), p->global_k);
         const ThrPlan tp = plan_rowthr(dtype, aligned, p->n, p->num_buckets, p->local_k, p->global_k);
         if (tp.ok) *bytes = std::max<size_t>(*bytes, rowthr_ws_bytes(rows, tp));
+        const StPlan sp = plan_streamthr(dtype, aligned, rows, p->n, p->num_buckets, p->local_k, p->global_k);
+        if (sp.ok) *bytes = std::max<size_t>(*bytes, sp.ws_bytes);
         break;
       }
       case ATKG_OP_SELECT:
@@ -700,6 +702,12 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     float* gv = reinterpret_cast<float*>(w);
     uint32_t* gi = reinterpret_cast<uint32_t*>(w + rows * gstride * 4);
     w += grid_bytes(rows, *p);
+    const StPlan sp = plan_streamthr(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
+    if (sp.ok) {  // long rows: threshold stream + per-row finish (exact fallback per row)
+      run_streamthr(dtype, sp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,
+                    reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(d_ws))), d_status, st);
+      return;
+    }
     const ThrPlan tp = plan_rowthr(dtype, d_in, p->n, p->num_buckets, p->local_k, p->global_k);
     if (tp.ok) {  // row-resident, row threshold: stage 1 + stage 2 in one warp per row
       run_rowthr(dtype, tp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,

@@ -69,4 +69,16 @@ uint64_t rowthr_ws_bytes(uint64_t rows, const ThrPlan& tp);
 void run_rowthr(int dtype, const ThrPlan& tp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
                 uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
 
+// threshold-stream approx_top_k for long rows (streamthr.cu)
+struct StPlan {
+  bool ok = false;
+  uint64_t vtot = 0, ws_bytes = 0;
+  uint32_t G = 0, smax = 1, slot_bytes = 32768, ns = 3, ecap = 4096;
+  float rfac = 0.f, lfac = 0.f;
+  size_t smem_stream = 0, smem_fin = 0;
+};
+StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k);
+void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
+                   uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
+
 }  // namespace atkg

@@ -1,0 +1,176 @@
+// streamthr.cu -- host planner + launchers of the threshold-stream
+// approx_top_k (streamthr.cuh) for long rows.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "internal.hpp"
+#include "streamthr.cuh"
+
+namespace atkg {
+
+namespace {
+
+uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::strtoull(e, nullptr, 10) : dflt;
+}
+
+// E[min(K', X)], X ~ Poisson(lambda)
+double mean_min_poisson(double lambda, uint32_t kp) {
+  double p = std::exp(-lambda), cdf = 0.0, m = 0.0;
+  for (uint32_t j = 0; j < kp; ++j) {
+    m += j * p;
+    cdf += p;
+    p *= lambda / (j + 1);
+  }
+  return m + kp * (1.0 - cdf);
+}
+
+// programmatic dependent launch: the kernel may start while the previous one
+// on the stream drains; it synchronises with griddepcontrol.wait before
+// touching what the previous kernel reads or writes
+template <typename K, typename A>
+void launch_pdl(K kern, unsigned grid, unsigned block, size_t smem, cudaStream_t st, const A& args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = env_u64("ATKG_NO_PDL", 0) ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_OK(cudaLaunchKernelEx(&cfg, kern, args));
+  check_launch();
+}
+
+template <typename T, int UNR>
+void launch_stream(const StPlan& sp, const StArgs& a, cudaStream_t st) {
+  auto kern = st_stream_kernel<T, UNR>;
+  static size_t attr = 0;
+  if (attr < sp.smem_stream) {
+    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem_stream));
+    attr = sp.smem_stream;
+  }
+  launch_pdl(kern, sp.G, kStNW * 32, sp.smem_stream, st, a);
+}
+
+template <typename T, int KP>
+void launch_finish(const StPlan& sp, uint64_t rows, const StFinArgs& a, cudaStream_t st) {
+  auto kern = st_finish_kernel<T, KP>;
+  static size_t attr = 0;
+  if (attr < sp.smem_fin) {
+    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem_fin));
+    attr = sp.smem_fin;
+  }
+  launch_pdl(kern, (unsigned)rows, 256, sp.smem_fin, st, a);
+}
+
+}  // namespace
+
+StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k) {
+  StPlan sp;
+  if (env_u64("ATKG_NO_STREAMTHR", 0)) return sp;
+  if (kp != 1 && kp != 2 && kp != 4 && kp != 8) return sp;
+  const uint64_t es = dtype == ATKG_BF16 ? 2 : 4;
+  const uint64_t ve = 16 / es;
+  if (n < env_u64("ATKG_STREAMTHR_MIN_N", 32768) || n > (1ull << 24) || n % ve != 0) return sp;
+  if (reinterpret_cast<uintptr_t>(in) % 16 != 0) return sp;
+  const uint64_t filled = std::min<uint64_t>(kp, n / B);
+  if (B > 4096 || B * filled > 8192 || k > B * filled) return sp;
+  sp.vtot = rows * n / ve;
+  if (sp.vtot >= (1ull << 50)) return sp;
+  if (sp.vtot / std::max<uint64_t>(1, (uint64_t)sm_count()) >= (1ull << 31)) return sp;  // 32-bit piece offsets
+  sp.slot_bytes = (uint32_t)env_u64("ATKG_ST_STEP", 32768);  // bytes per CTA step
+  if (sp.slot_bytes != 16384 && sp.slot_bytes != 32768) return sp;
+  sp.ns = 0;
+  const uint64_t per_sm = env_u64("ATKG_ST_CTAS", 2);
+  uint64_t G = (uint64_t)sm_count() * per_sm;
+  G = std::max<uint64_t>(1, std::min<uint64_t>(G, sp.vtot / 1024));
+  sp.G = (uint32_t)G;
+  // rows spanned by any piece
+  const uint64_t nvrow = n / ve;
+  uint64_t smax = 1;
+  for (uint32_t c = 0; c < sp.G; ++c) {
+    const uint64_t v0 = st_piece_start(sp.vtot, sp.G, c), v1 = st_piece_start(sp.vtot, sp.G, c + 1);
+    if (v1 > v0) smax = std::max<uint64_t>(smax, (v1 - 1) / nvrow - v0 / nvrow + 1);
+  }
+  sp.smax = (uint32_t)smax;
+  if (sp.G > kStMaxRowPieces) return sp;
+  // target count T of row elements >= L: B * E[min(K', Poisson(T/B))] must
+  // clear K with margin; every warp sub-stream keeps ~2x its share of T
+  const double need = 1.2 * k + 4.0 * std::sqrt((double)k) + 8.0;
+  double T = 1.0;
+  while (T < (double)n && (double)B * mean_min_poisson(T / (double)B, kp) < need) T *= 1.05;
+  sp.rfac = (float)(2.0 * T / (double)n);
+  sp.lfac = (float)(T / 1.5 / (double)n);
+  // gathered entries per row: ~T, but up to ~2.4 per warp sub-stream when a
+  // few rows are cut into many pieces (the max of many sub-stream thresholds)
+  uint64_t ecap = rows >= 64 ? 4096 : 8192;
+  while (ecap < B * filled) ecap <<= 1;
+  sp.ecap = (uint32_t)ecap;
+  sp.smem_stream = (size_t)kStNW * 2 * kStLog * 4 + (size_t)kStSlots * sp.slot_bytes;  // logs | per-warp rings
+  sp.smem_fin = (size_t)ecap * 16 + (size_t)B * 12;
+  if (sp.smem_stream > 220 * 1024 || sp.smem_fin > 220 * 1024) return sp;
+  sp.ws_bytes = (uint64_t)sp.G * sp.smax * kStNW * kStSlotWords * 4;
+  sp.ok = true;
+  return sp;
+}
+
+void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
+                   uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st) {
+  StArgs a;
+  a.in = in;
+  a.n = n;
+  a.vtot = sp.vtot;
+  a.G = sp.G;
+  a.smax = sp.smax;
+  a.slot_bytes = sp.slot_bytes;
+  a.ns = sp.ns;
+  a.rfac = sp.rfac;
+  a.lfac = sp.lfac;
+  a.slots = static_cast<uint32_t*>(ws);
+  a.status = status;
+  StFinArgs f;
+  f.in = in;
+  f.n = n;
+  f.vtot = sp.vtot;
+  f.G = sp.G;
+  f.smax = sp.smax;
+  f.B = (uint32_t)B;
+  f.k = k;
+  f.ecap = sp.ecap;
+  f.slots = static_cast<const uint32_t*>(ws);
+  f.out_v = ov;
+  f.out_i = oi;
+  f.status = status;
+  f.force_slow = (uint32_t)env_u64("ATKG_ST_FORCE_SLOW", 0);
+  g_prof.bracket_begin(st);
+  if (dtype == ATKG_BF16) {
+    if (sp.slot_bytes == 32768) launch_stream<__nv_bfloat16, 8>(sp, a, st);
+    else launch_stream<__nv_bfloat16, 4>(sp, a, st);
+  } else {
+    if (sp.slot_bytes == 32768) launch_stream<float, 8>(sp, a, st);
+    else launch_stream<float, 4>(sp, a, st);
+  }
+  g_prof.bracket_end(st);
+#define ATKG_ST_FIN(T_)                                   \
+  switch (kp) {                                           \
+    case 1: launch_finish<T_, 1>(sp, rows, f, st); break; \
+    case 2: launch_finish<T_, 2>(sp, rows, f, st); break; \
+    case 4: launch_finish<T_, 4>(sp, rows, f, st); break; \
+    default: launch_finish<T_, 8>(sp, rows, f, st); break; \
+  }
+  if (dtype == ATKG_BF16) {
+    ATKG_ST_FIN(__nv_bfloat16)
+  } else {
+    ATKG_ST_FIN(float)
+  }
+#undef ATKG_ST_FIN
+}
+
+}  // namespace atkg
