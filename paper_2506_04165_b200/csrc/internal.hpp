@@ -72,7 +72,7 @@ void run_rowthr(int dtype, const ThrPlan& tp, const void* in, uint64_t rows, uin
 // threshold-stream approx_top_k for long rows (streamthr.cu)
 struct StPlan {
   bool ok = false;
-  uint64_t vtot = 0, ws_bytes = 0;
+  uint64_t vtot = 0, psz = 0, ws_bytes = 0;
   uint32_t G = 0, smax = 1, slot_bytes = 32768, ns = 3, ecap = 4096;
   float rfac = 0.f, lfac = 0.f;
   size_t smem_stream = 0, smem_fin = 0;

@@ -91,16 +91,16 @@ StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint
   const uint64_t per_sm = env_u64("ATKG_ST_CTAS", 2);
   uint64_t G = (uint64_t)sm_count() * per_sm;
   G = std::max<uint64_t>(1, std::min<uint64_t>(G, sp.vtot / 1024));
-  sp.G = (uint32_t)G;
+  sp.psz = (sp.vtot + G - 1) / G;
+  sp.G = (uint32_t)((sp.vtot + sp.psz - 1) / sp.psz);
   // rows spanned by any piece
   const uint64_t nvrow = n / ve;
   uint64_t smax = 1;
   for (uint32_t c = 0; c < sp.G; ++c) {
-    const uint64_t v0 = st_piece_start(sp.vtot, sp.G, c), v1 = st_piece_start(sp.vtot, sp.G, c + 1);
+    const uint64_t v0 = st_piece_start(sp.vtot, sp.psz, c), v1 = st_piece_start(sp.vtot, sp.psz, c + 1);
     if (v1 > v0) smax = std::max<uint64_t>(smax, (v1 - 1) / nvrow - v0 / nvrow + 1);
   }
   sp.smax = (uint32_t)smax;
-  if (sp.G > kStMaxRowPieces) return sp;
   // target count T of row elements >= L: B * E[min(K', Poisson(T/B))] must
   // clear K with margin; every warp sub-stream keeps ~2x its share of T
   const double need = 1.2 * k + 4.0 * std::sqrt((double)k) + 8.0;
@@ -127,6 +127,7 @@ void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, u
   a.in = in;
   a.n = n;
   a.vtot = sp.vtot;
+  a.psz = sp.psz;
   a.G = sp.G;
   a.smax = sp.smax;
   a.slot_bytes = sp.slot_bytes;
@@ -139,6 +140,7 @@ void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, u
   f.in = in;
   f.n = n;
   f.vtot = sp.vtot;
+  f.psz = sp.psz;
   f.G = sp.G;
   f.smax = sp.smax;
   f.B = (uint32_t)B;

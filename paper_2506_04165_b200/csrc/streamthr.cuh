@@ -77,6 +77,7 @@ struct StArgs {
   const void* in;
   uint64_t n;          // row length
   uint64_t vtot;       // 16-byte vectors in the whole input
+  uint64_t psz;        // vectors per piece
   uint32_t G;          // pieces (= grid)
   uint32_t smax;       // slot segments per piece
   uint32_t slot_bytes; // ring slot size
@@ -87,8 +88,10 @@ struct StArgs {
   uint32_t* status;
 };
 
-__host__ __device__ __forceinline__ uint64_t st_piece_start(uint64_t vtot, uint32_t G, uint32_t c) {
-  return vtot * c / G;  // vtot * G < 2^64 (host-checked)
+// piece c = vectors [c * psz, min(vtot, (c + 1) * psz))
+__host__ __device__ __forceinline__ uint64_t st_piece_start(uint64_t vtot, uint64_t psz, uint32_t c) {
+  const uint64_t v = psz * c;
+  return v < vtot ? v : vtot;
 }
 
 // warp: the r-th largest of the n logged keys (n >= r >= 1), by MSB-first
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(kStNW * 32, 2) st_stream_kernel(StArgs a) {
   __shared__ __align__(8) uint64_t full_bar[kStNW][kStSlots];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t c = blockIdx.x;
-  const uint64_t v0 = st_piece_start(a.vtot, a.G, c), v1 = st_piece_start(a.vtot, a.G, c + 1);
+  const uint64_t v0 = st_piece_start(a.vtot, a.psz, c), v1 = st_piece_start(a.vtot, a.psz, c + 1);
   const uint64_t nvrow = a.n / VE;  // vectors per row
   const uint4* in = static_cast<const uint4*>(a.in);
   uint4* ring = reinterpret_cast<uint4*>(st_smem + (size_t)kStNW * 2 * kStLog * 4) + warp * kStSlots * WV;
@@ -487,9 +490,79 @@ __global__ void __launch_bounds__(kStNW * 32, 2) st_stream_kernel(StArgs a) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Emits the first k (ascending) of M unique 64-bit keys: bins on the high
+// word (ascending with the key), a counting sort into `mem` (M u64, 8-byte
+// aligned), ranks inside a bin by comparison.  Block-wide; returns false
+// (nothing written) when a bin is too crowded -- the caller sorts instead.
+__device__ __forceinline__ bool st_emit_ranked(const uint64_t* keys, uint32_t* mem32, uint32_t M, uint32_t k,
+                                               float* ov, uint32_t* oi) {
+  constexpr uint32_t NB = 256, RUN = 48;
+  __shared__ uint32_t hlo, hhi, hist[NB + 1], curs[NB], hmax;
+  uint64_t* mem = reinterpret_cast<uint64_t*>(mem32);
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
+  if (t == 0) { hlo = 0xffffffffu; hhi = 0; hmax = 0; }
+  for (uint32_t b = t; b <= NB; b += nt) hist[b] = 0;
+  __syncthreads();
+  uint32_t lo = 0xffffffffu, hi = 0;
+  for (uint32_t q = t; q < M; q += nt) {
+    const uint32_t h = (uint32_t)(keys[q] >> 32);
+    lo = min(lo, h);
+    hi = max(hi, h);
+  }
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if ((t & 31) == 0) { atomicMin(&hlo, lo); atomicMax(&hhi, hi); }
+  __syncthreads();
+  lo = hlo;
+  const uint32_t span = hhi - lo;
+  const uint32_t shift = span < NB ? 0u : (uint32_t)(32 - __clz((int)(span >> 8)));  // span >> shift < NB
+  auto bin = [&](uint64_t key) { return ((uint32_t)(key >> 32) - lo) >> shift; };
+  for (uint32_t q = t; q < M; q += nt) atomicAdd(&hist[bin(keys[q])], 1u);
+  __syncthreads();
+  if (t < 32) {  // exclusive scan of NB bins, 8 per lane
+    uint32_t c[NB / 32], tot = 0, mx = 0;
+#pragma unroll
+    for (int i = 0; i < (int)(NB / 32); ++i) { c[i] = hist[t * (NB / 32) + i]; tot += c[i]; mx = max(mx, c[i]); }
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((int)t >= o) incl += y;
+    }
+    uint32_t ex = incl - tot;
+#pragma unroll
+    for (int i = 0; i < (int)(NB / 32); ++i) {
+      hist[t * (NB / 32) + i] = ex;
+      curs[t * (NB / 32) + i] = ex;
+      ex += c[i];
+    }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (t == 0) { hist[NB] = M; hmax = mx; }
+  }
+  __syncthreads();
+  if (hmax > RUN) return false;  // uniform
+  for (uint32_t q = t; q < M; q += nt) {
+    const uint64_t key = keys[q];
+    mem[atomicAdd(&curs[bin(key)], 1u)] = key;
+  }
+  __syncthreads();
+  for (uint32_t q = t; q < M; q += nt) {
+    const uint64_t key = mem[q];
+    const uint32_t b = bin(key);
+    const uint32_t b0 = hist[b], b1 = hist[b + 1];
+    uint32_t r = b0;
+    for (uint32_t o = b0; o < b1; ++o) r += mem[o] < key ? 1u : 0u;
+    if (r < k) {
+      ov[r] = __uint_as_float(key_value_bits(key));
+      oi[r] = (uint32_t)key;
+    }
+  }
+  return true;
+}
+
 struct StFinArgs {
   const void* in;
-  uint64_t n, vtot;
+  uint64_t n, vtot, psz;
   uint32_t G, smax, B, k;
   uint32_t ecap;   // gathered-entry capacity (shared memory)
   uint32_t force_slow;  // tests: every row takes the exact fallback
@@ -506,7 +579,7 @@ template <typename T, int KP>
 __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
   extern __shared__ __align__(128) uint8_t st_smem[];
   uint8_t* smem = st_smem;
-  __shared__ uint32_t sh_l, sh_ne, sh_bad, sh_nc, sh_m;
+  __shared__ uint32_t sh_l, sh_ne, sh_nk, sh_bad, sh_nc, sh_m;
   __shared__ uint64_t red64[16];
   const uint32_t t = threadIdx.x, nt = blockDim.x;
   const uint64_t row = blockIdx.x;
@@ -523,73 +596,72 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
   const uint32_t B = a.B;
   const bool pow2 = (B & (B - 1)) == 0;
   auto bucket = [&](uint32_t p) { return pow2 ? (p & (B - 1)) : p % B; };  // partition_index, topk.hpp:13-15
-  if (t == 0) { sh_l = 0; sh_ne = 0; sh_bad = 0; sh_nc = 0; }
+  if (t == 0) { sh_l = 0; sh_ne = 0; sh_nk = 0; sh_bad = 0; sh_nc = 0; }
   for (uint32_t b = t; b < B; b += nt) cnt[b] = 0;
-  // pieces overlapping this row (thread 0), and the row's segment index in
-  // each of them
-  __shared__ uint32_t sh_ca, sh_cb;
-  __shared__ uint16_t segi[kStMaxRowPieces];
-  if (t == 0) {
-    const uint64_t va = row * nvrow, vb = (row + 1) * nvrow - 1;
-    auto piece_of = [&](uint64_t v) {
-      uint32_t c = (uint32_t)(v * a.G / a.vtot);
-      while (c + 1 < a.G && st_piece_start(a.vtot, a.G, c + 1) <= v) ++c;
-      while (c > 0 && st_piece_start(a.vtot, a.G, c) > v) --c;
-      return c;
-    };
-    sh_ca = piece_of(va);
-    sh_cb = piece_of(vb);
-  }
-  __syncthreads();
-  const uint32_t ca = sh_ca, cb = sh_cb;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the stream kernel's slots are complete
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  for (uint32_t q = t; q <= cb - ca; q += nt) segi[q] = (uint16_t)(row - st_piece_start(a.vtot, a.G, ca + q) / nvrow);
+  // pieces overlapping this row; the row is segment 0 of every piece but
+  // the first (those start inside the row)
+  const uint64_t va = row * nvrow, vb = (row + 1) * nvrow - 1;
+  const uint32_t ca = (uint32_t)(va / a.psz), cb = (uint32_t)(vb / a.psz);
+  const uint32_t seg_a = (uint32_t)(row - (uint64_t)ca * a.psz / nvrow);
   const uint32_t nslots = (cb - ca + 1) * kStNW;
-  __syncthreads();
   auto slot_ptr = [&](uint32_t q) {
     const uint32_t c = ca + q / kStNW, w = q % kStNW;
-    return a.slots + (((uint64_t)c * a.smax + segi[q / kStNW]) * kStNW + w) * kStSlotWords;
+    return a.slots + (((uint64_t)c * a.smax + (c == ca ? seg_a : 0u)) * kStNW + w) * kStSlotWords;
   };
+  __syncthreads();  // counters initialised
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the stream kernel's slots are complete
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // gather every slot's entries (one warp per slot; header and the first 64
+  // entries in one round trip), the row threshold L = max of slot thresholds
+  const int lane = t & 31, wq = t >> 5;
   uint32_t lmax = 0;
-  for (uint32_t q = t; q < nslots; q += nt) {
+  for (uint32_t q = wq; q < nslots; q += nt / 32) {
     const uint32_t* sl = slot_ptr(q);
-    lmax = max(lmax, sl[1]);
-    if (sl[0] > kStSlotCap) atomicOr(&sh_bad, 1u);
-  }
-  atomicMax(&sh_l, lmax);
-  __syncthreads();
-  const uint32_t Lk = sh_l;
-  bool fast = sh_bad == 0 && Lk > kStKeyNegInf && !a.force_slow;
-  if (fast) {
-    // gather the entries >= L (one warp per slot)
-    const int lane = t & 31, w = t >> 5;
-    for (uint32_t q = w; q < nslots; q += nt / 32) {
-      const uint32_t* sl = slot_ptr(q);
-      const uint32_t m = sl[0];
-      for (uint32_t e0 = 0; e0 < m; e0 += 32) {  // m is uniform across the warp
-        const uint32_t e = e0 + lane;
-        const uint32_t key = e < m ? sl[2 + e] : 0u;
-        const bool keep = e < m && key >= Lk;
-        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-        uint32_t base = 0;
-        if (lane == 0 && bal) base = atomicAdd(&sh_ne, __popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (keep) {
-          const uint32_t d = base + __popc(bal & ((1u << lane) - 1u));
-          if (d < a.ecap) {
-            const uint32_t p = sl[2 + kStSlotCap + e];
-            ek[d] = key;
-            ep[d] = p;
-            atomicAdd(&cnt[bucket(p)], 1u);
-          }
-        }
+    const uint32_t hdr = lane < 2 ? sl[lane] : 0u;
+    uint32_t kk[2], pp[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      kk[h] = sl[2 + h * 32 + lane];
+      pp[h] = sl[2 + kStSlotCap + h * 32 + lane];
+    }
+    const uint32_t m = __shfl_sync(0xffffffffu, hdr, 0);
+    lmax = max(lmax, __shfl_sync(0xffffffffu, hdr, 1));
+    if (m > kStSlotCap) {
+      if (lane == 0) sh_bad = 1u;
+      continue;
+    }
+    uint32_t base = 0;
+    if (lane == 0 && m) base = atomicAdd(&sh_ne, m);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (uint32_t e0 = 0; e0 < m; e0 += 32) {
+      const uint32_t e = e0 + lane;
+      uint32_t key, pos;
+      if (e0 < 64) {
+        key = e0 == 0 ? kk[0] : kk[1];
+        pos = e0 == 0 ? pp[0] : pp[1];
+      } else {
+        key = e < m ? sl[2 + e] : 0u;
+        pos = e < m ? sl[2 + kStSlotCap + e] : 0u;
+      }
+      if (e < m && base + e < a.ecap) {
+        ek[base + e] = key;
+        ep[base + e] = pos;
       }
     }
+  }
+  if (lmax) atomicMax(&sh_l, lmax);
+  __syncthreads();
+  const uint32_t Lk = sh_l, ne_all = sh_ne;
+  bool fast = sh_bad == 0 && Lk > kStKeyNegInf && !a.force_slow && ne_all <= a.ecap;
+  if (fast) {
+    uint32_t nk = 0;
+    for (uint32_t q = t; q < ne_all; q += nt)
+      if (ek[q] >= Lk) { atomicAdd(&cnt[bucket(ep[q])], 1u); ++nk; }
+    nk = __reduce_add_sync(0xffffffffu, nk);
+    if (lane == 0 && nk) atomicAdd(&sh_nk, nk);
     __syncthreads();
-    const uint32_t ne = sh_ne;
-    fast = ne <= a.ecap;
-    if (fast) {
+    const uint32_t ne = sh_nk;
+    {
       // M and bucket offsets (block scan over buckets; thread owns a run)
       const uint32_t per = (B + nt - 1) / nt;
       const uint32_t b0 = min(B, t * per), b1 = min(B, b0 + per);
@@ -601,7 +673,8 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
       for (uint32_t b = b0; b < b1; ++b) { off[b] = o; cur[b] = o; o += cnt[b]; }
       if (t == 0) sh_m = (uint32_t)(tot >> 32);
       __syncthreads();
-      for (uint32_t q = t; q < ne; q += nt) {
+      for (uint32_t q = t; q < ne_all; q += nt) {
+        if (ek[q] < Lk) continue;
         const uint32_t d = atomicAdd(&cur[bucket(ep[q])], 1u);
         gk[d] = ek[q];
         gp[d] = ep[q];
@@ -669,20 +742,11 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
   while (P < M) P <<= 1;
   for (uint32_t q = M + t; q < P; q += nt) cand[q] = ~0ull;
   __syncthreads();
-  if (fast && M <= 1024) {
-    // unique keys (real elements >= L > -inf): rank = #smaller keys (broadcast shared-memory reads, no
-    // barriers); the first k ranks are the output
-    for (uint32_t q = t; q < M; q += nt) {
-      const uint64_t key = cand[q];
-      uint32_t r = 0;
-#pragma unroll 4
-      for (uint32_t o = 0; o < M; ++o) r += cand[o] < key ? 1u : 0u;
-      if (r < a.k) {
-        a.out_v[row * a.k + r] = __uint_as_float(key_value_bits(key));
-        a.out_i[row * a.k + r] = (uint32_t)key;
-      }
-    }
-    return;
+  if (fast) {
+    // unique keys (real elements >= L > -inf): counting sort on the key's
+    // value word (ascending = value descending), ranks inside a bin by
+    // comparison; the first k ranks are the output
+    if (st_emit_ranked(cand, gk, M, a.k, a.out_v + row * a.k, a.out_i + row * a.k)) return;
   }
   group_bitonic_sort<uint64_t>(cand, P, t, nt);
   for (uint32_t q = t; q < a.k; q += nt) {

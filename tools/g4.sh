@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_streamthr.py -m gpu -x -q > gpurun_out/t_st.log 2>&1; echo rc=$? >> gpurun_out/t_st.log
+timeout 300 python tools/quick_time.py C2 C1 > gpurun_out/q_st.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:st_ --csv python tools/quick_time.py C2 > gpurun_out/st_launch.csv 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:st_finish -s 2 -c 1 -o gpurun_out/prof_fin -f python tools/quick_time.py C2 > gpurun_out/ncu_fin.log 2>&1
