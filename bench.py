@@ -241,11 +241,20 @@ class RowsWorkload:
     def hbm_bytes(self):
         return self.rows * self.n * self.esz
 
+    def dominant_kernel(self):
+        # the approx_top_k plan (csrc/atkg_api.cu): long rows take the threshold
+        # stream (streamthr.cuh), rows that fit in shared memory the row-resident path
+        if self.n >= 32768 and not os.environ.get("ATKG_NO_STREAMTHR"):
+            return "st_stream_kernel (threshold stream; stage-1 pass)"
+        if self.n * self.esz <= 64 * 1024:
+            return "row_threshold_kernel" if self.kp >= 8 else "row_resident_kernel"
+        return self.kernel
+
     def roofline(self, kern_ms, ms_step):
         peak, src = peaks()
         alg = self.rows * self.n * self.esz + self.rows * self.b * self.kp * 8
         ach = alg / (kern_ms * 1e-3) / 1e9
-        return {"kernel": self.kernel, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+        return {"kernel": self.dominant_kernel(), "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
                 "peak_source": src, "unit": "GB/s", "frac": round(ach / peak, 4),
                 "traffic": traffic_from_profiles(self.args.config), "alg_bytes_per_launch": alg,
                 "launch_ms": round(kern_ms, 5), "share_of_step": round(kern_ms / ms_step, 4)}
