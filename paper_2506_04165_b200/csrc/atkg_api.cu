@@ -708,6 +708,11 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
                     reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(d_ws))), d_status, st);
       return;
     }
+    const PipePlan pp = plan_rowpipe(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
+    if (pp.ok) {  // bf16 rows in shared memory: persistent row pipeline, row threshold
+      run_rowpipe(pp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx, d_status, st);
+      return;
+    }
     const ThrPlan tp = plan_rowthr(dtype, d_in, p->n, p->num_buckets, p->local_k, p->global_k);
     if (tp.ok) {  // row-resident, row threshold: stage 1 + stage 2 in one warp per row
       run_rowthr(dtype, tp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,

@@ -69,6 +69,16 @@ uint64_t rowthr_ws_bytes(uint64_t rows, const ThrPlan& tp);
 void run_rowthr(int dtype, const ThrPlan& tp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
                 uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
 
+// persistent row pipeline for bf16 rows in shared memory (rowpipe.cu)
+struct PipePlan {
+  bool ok = false;
+  uint32_t cap = 512, rsel = 1, slot_bytes = 0, scr_words = 0, grid = 1;
+  size_t smem = 0;
+};
+PipePlan plan_rowpipe(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k);
+void run_rowpipe(const PipePlan& pp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
+                 float* ov, uint32_t* oi, uint32_t* status, cudaStream_t st);
+
 // threshold-stream approx_top_k for long rows (streamthr.cu)
 struct StPlan {
   bool ok = false;
