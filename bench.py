@@ -509,7 +509,9 @@ class GiantRowWorkload(RowsWorkload):
         peak, src = peaks()
         alg = self.length * 4 + self.b * self.kp * 8
         ach = alg / (kern_ms * 1e-3) / 1e9
-        return {"kernel": self.kernel, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+        kern = ("stage1_flat_kernel (slice summaries)" if self.sharded is not None
+                else "st_stream_kernel (threshold stream; stage-1 pass)")
+        return {"kernel": kern, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
                 "peak_source": src, "unit": "GB/s", "frac": round(ach / peak, 4),
                 "traffic": traffic_from_profiles("C5"), "alg_bytes_per_launch": alg,
                 "launch_ms": round(kern_ms, 5), "share_of_step": round(kern_ms / ms_step, 4)}

@@ -704,9 +704,16 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     w += grid_bytes(rows, *p);
     const StPlan sp = plan_streamthr(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
     if (sp.ok) {  // long rows: threshold stream + per-row finish (exact fallback per row)
+      void* sws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(d_ws)));
       run_streamthr(dtype, sp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,
-                    reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(d_ws))), d_status, st);
-      return;
+                    sws, d_status, st);
+      if (!sp.giant) return;
+      // giant rows: read the gate (4 bytes) and rerun the exact path if a
+      // row's threshold failed (the device cannot afford that fallback)
+      uint32_t gate = 0;
+      CUDA_OK(cudaMemcpyAsync(&gate, static_cast<char*>(sws) + (sp.ws_bytes - 256), 4, cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaStreamSynchronize(st));
+      if (!gate) return;
     }
     const PipePlan pp = plan_rowpipe(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
     if (pp.ok) {  // bf16 rows in shared memory: persistent row pipeline, row threshold

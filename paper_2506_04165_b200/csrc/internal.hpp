@@ -81,10 +81,10 @@ void run_rowpipe(const PipePlan& pp, const void* in, uint64_t rows, uint64_t n, 
 
 // threshold-stream approx_top_k for long rows (streamthr.cu)
 struct StPlan {
-  bool ok = false;
+  bool ok = false, giant = false;
   uint64_t vtot = 0, psz = 0, ws_bytes = 0;
   uint32_t G = 0, smax = 1, slot_bytes = 32768, ns = 3, ecap = 4096;
-  float rfac = 0.f, lfac = 0.f;
+  float rfac = 0.f, lfac = 0.f, cfac = 0.f;
   size_t smem_stream = 0, smem_fin = 0;
 };
 StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k);

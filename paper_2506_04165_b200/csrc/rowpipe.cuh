@@ -240,7 +240,8 @@ __global__ void __launch_bounds__(B * NG, 1) row_pipe_kernel(PipeArgs a) {
       for (int w2 = 0; w2 < B / 32; ++w2) { lo = min(lo, red[33 + w2]); hi = max(hi, red[33 + B / 32 + w2]); }
       // bin = (value code - lo) * kPipeSub + index quarter: ascending bins =
       // ascending keys, a bin holds equal values from one quarter of the row
-      const uint32_t sub_shift = (uint32_t)max(0, 32 - __clz((int)(a.n - 1)) - 2);
+      static_assert(kPipeSub == 1 || kPipeSub == 2 || kPipeSub == 4, "index sub-bins");
+      const uint32_t sub_shift = (uint32_t)max(0, 32 - __clz((int)(a.n - 1)) - (kPipeSub == 4 ? 2 : kPipeSub == 2 ? 1 : 0));
       auto bin = [&](uint32_t key) { return ((key >> 16) - lo) * kPipeSub + ((key & 0xffffu) >> sub_shift); };
       if ((hi - lo) * kPipeSub < (uint32_t)kPipeNB) {  // group-uniform
         for (uint32_t qq = t; qq < M; qq += B) atomicAdd(&hist[bin(keys[qq])], 1u);

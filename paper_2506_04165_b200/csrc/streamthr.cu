@@ -78,7 +78,11 @@ StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint
   if (kp != 1 && kp != 2 && kp != 4 && kp != 8) return sp;
   const uint64_t es = dtype == ATKG_BF16 ? 2 : 4;
   const uint64_t ve = 16 / es;
-  if (n < env_u64("ATKG_STREAMTHR_MIN_N", 32768) || n > (1ull << 24) || n % ve != 0) return sp;
+  if (n < env_u64("ATKG_STREAMTHR_MIN_N", 32768) || n % ve != 0) return sp;
+  // rows beyond 2^24 elements (the giant row) do not take the in-kernel exact
+  // fallback; a failed row is flagged and rerun on the exact path by the host
+  sp.giant = n > env_u64("ATKG_ST_GIANT_N", 1ull << 24);
+  if (n > 0xffffffffull) return sp;
   if (reinterpret_cast<uintptr_t>(in) % 16 != 0) return sp;
   const uint64_t filled = std::min<uint64_t>(kp, n / B);
   if (B > 4096 || B * filled > 8192 || k > B * filled) return sp;
@@ -108,6 +112,10 @@ StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint
   while (T < (double)n && (double)B * mean_min_poisson(T / (double)B, kp) < need) T *= 1.05;
   sp.rfac = (float)(2.0 * T / (double)n);
   sp.lfac = (float)(T / 1.5 / (double)n);
+  // rows cut into many pieces (the giant row): cap each slot at ~3x its share
+  // of T, else the row threshold (max over the slots) gathers too much;
+  // rows over a few pieces never need it (a slot holds <= 8 * kStWarpCap)
+  sp.cfac = (n / ve > 8 * sp.psz) ? (float)(3.0 * T / (double)n) : 1e30f;
   // gathered entries per row: ~T, but up to ~2.4 per warp sub-stream when a
   // few rows are cut into many pieces (the max of many sub-stream thresholds)
   uint64_t ecap = rows >= 64 ? 4096 : 8192;
@@ -116,7 +124,8 @@ StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint
   sp.smem_stream = (size_t)kStNW * 2 * kStLog * 4 + (size_t)kStSlots * sp.slot_bytes;  // logs | per-warp rings
   sp.smem_fin = (size_t)ecap * 16 + (size_t)B * 12;
   if (sp.smem_stream > 220 * 1024 || sp.smem_fin > 220 * 1024) return sp;
-  sp.ws_bytes = (uint64_t)sp.G * sp.smax * kStNW * kStSlotWords * 4;
+  if (sp.G > kStMaxRowPieces) return sp;
+  sp.ws_bytes = (uint64_t)sp.G * sp.smax * kStSlotWords * 4 + 256;  // slots | gate
   sp.ok = true;
   return sp;
 }
@@ -134,7 +143,10 @@ void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, u
   a.ns = sp.ns;
   a.rfac = sp.rfac;
   a.lfac = sp.lfac;
+  a.cfac = sp.cfac;
   a.slots = static_cast<uint32_t*>(ws);
+  uint32_t* gate = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + (sp.ws_bytes - 256));
+  a.gate = sp.giant ? gate : nullptr;
   a.status = status;
   StFinArgs f;
   f.in = in;
@@ -151,6 +163,7 @@ void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, u
   f.out_i = oi;
   f.status = status;
   f.force_slow = (uint32_t)env_u64("ATKG_ST_FORCE_SLOW", 0);
+  f.gate = a.gate;
   g_prof.bracket_begin(st);
   if (dtype == ATKG_BF16) {
     if (sp.slot_bytes == 32768) launch_stream<__nv_bfloat16, 8>(sp, a, st);

@@ -46,7 +46,8 @@ namespace atkg {
 
 constexpr int kStNW = 8;           // consumer warps per CTA
 constexpr uint32_t kStLog = 256;   // log entries per warp
-constexpr uint32_t kStSlotCap = 128;  // entries per flushed slot
+constexpr uint32_t kStWarpCap = 128;  // entries a warp keeps at a flush
+constexpr uint32_t kStSlotCap = 1024;  // entries per (piece, row segment) slot
 constexpr uint32_t kStSlotWords = 2 + 2 * kStSlotCap;  // {count, Lkey} | keys | positions
 constexpr uint32_t kStBadCount = 0xffffffffu;
 constexpr uint32_t kStMaxRowPieces = 2048;  // pieces one row may span (host-checked)
@@ -84,7 +85,9 @@ struct StArgs {
   uint32_t ns;         // ring slots
   float rfac;          // per-warp rank target: R = 8 + rfac * (warp share of the segment)
   float lfac;          // sampled start: expected sample count above the row's safe level, per element
-  uint32_t* slots;     // [G][smax][kStNW][kStSlotWords]
+  float cfac;          // entries kept per row segment: Rc = 8 + cfac * (segment elements)
+  uint32_t* slots;     // [G][smax][kStSlotWords]
+  uint32_t* gate;      // giant rows: set by the finish kernel when a row needs the exact path
   uint32_t* status;
 };
 
@@ -237,14 +240,9 @@ __device__ __forceinline__ void st_log_vec(StWarp& w, uint4 x, uint32_t pbase, i
 }
 
 // flush a segment's log to its slot {count | kStBadCount, Lkey, keys, positions}
-__device__ __noinline__ void st_flush(StWarp& w, uint32_t* sl, int lane) {
-  if (w.n > kStSlotCap) w.n = st_warp_compact(w.keys, w.poss, w.n, w.r, kStSlotCap, w.tkey, lane);
-  if (lane == 0) { sl[0] = (w.bad || w.n > kStSlotCap) ? kStBadCount : w.n; sl[1] = w.tkey; }
-  for (uint32_t q = lane; q < w.n; q += 32) {
-    sl[2 + q] = w.keys[q];
-    sl[2 + kStSlotCap + q] = w.poss[q];
-  }
-  __syncwarp();
+__device__ __noinline__ void st_warp_trim(StWarp& w, int lane) {
+  if (w.n > kStWarpCap) w.n = st_warp_compact(w.keys, w.poss, w.n, w.r, kStWarpCap, w.tkey, lane);
+  if (w.n > kStWarpCap) w.bad = 1u;
 }
 
 // warp: the s-th largest of the CTA's 32 * kStNW sampled keys (bisection)
@@ -305,7 +303,12 @@ __global__ void __launch_bounds__(kStNW * 32, 2) st_stream_kernel(StArgs a) {
   __shared__ uint32_t samp[kStNW * 32];
   __shared__ uint32_t wcnt[kStNW];
   __shared__ __align__(8) uint64_t full_bar[kStNW][kStSlots];
+  __shared__ uint32_t fl_l[kStNW], fl_n[kStNW], fl_ctr, fl_bad;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    fl_ctr = 0;
+    fl_bad = 0;
+  }
   const uint32_t c = blockIdx.x;
   const uint64_t v0 = st_piece_start(a.vtot, a.psz, c), v1 = st_piece_start(a.vtot, a.psz, c + 1);
   const uint64_t nvrow = a.n / VE;  // vectors per row
@@ -322,6 +325,7 @@ __global__ void __launch_bounds__(kStNW * 32, 2) st_stream_kernel(StArgs a) {
   // PDL: the launch overlaps the previous kernel's tail; wait for its
   // completion (and memory) before reading the input or writing slots
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.gate) *a.gate = 0u;
   if (lane == 0) {
     for (int s = 0; s < kStSlots; ++s) ptx::mbar_init(&full_bar[warp][s], 1);
     ptx::fence_mbar_init();
@@ -353,8 +357,72 @@ __global__ void __launch_bounds__(kStNW * 32, 2) st_stream_kernel(StArgs a) {
     ptx::mbar_arrive_expect_tx(&full_bar[warp][s], wl * 16);
     if (wl) ptx::bulk_g2s(ring + s * WV, in + v0 + st.cur + warp * WV, wl * 16, &full_bar[warp][s], pol);
   };
+  uint32_t seg_len_e = 0;  // elements of the current row segment in this piece
+  // CTA-level flush of a row segment (uniform over the CTA): Lc = max of the
+  // warps' thresholds; every warp appends its entries >= Lc to the slot
   auto flush = [&](uint32_t seg) {  // seg = row - row0
-    st_flush(w, a.slots + (((uint64_t)c * a.smax + seg) * kStNW + warp) * kStSlotWords, lane);
+    st_warp_trim(w, lane);
+    if (lane == 0) {
+      fl_l[warp] = w.tkey;
+      fl_n[warp] = w.n;
+      if (w.bad) fl_bad = 1u;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kStNW * 32) : "memory");
+    uint32_t Lc = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < kStNW; ++i) { Lc = max(Lc, fl_l[i]); tot += fl_n[i]; }
+    // keep about Rc entries per segment: when the warps logged far more
+    // (a row cut into many pieces), warp 0 raises Lc to the Rc-th largest
+    // logged key (16-bit prefix bisection; any Lc above the warps' own
+    // thresholds keeps the slot exact)
+    const uint32_t Rc = (uint32_t)fminf(768.f, 8.f + ceilf(fminf(1e6f, a.cfac * (float)seg_len_e)));
+    if (tot > 2 * Rc) {  // uniform
+      if (warp == 0) {
+        const uint32_t* lk = reinterpret_cast<const uint32_t*>(st_smem);
+        uint32_t ans = 0;
+#pragma unroll 1
+        for (int bit = 31; bit >= 16; --bit) {
+          const uint32_t cand = ans | (1u << bit);
+          uint32_t cnt = 0;
+          for (int i = 0; i < kStNW; ++i) {
+            const uint32_t* kk = lk + i * 2 * kStLog;
+            const uint32_t ni = fl_n[i];
+            for (uint32_t e = lane; e < ni; e += 32) cnt += kk[e] >= cand ? 1u : 0u;
+          }
+          if (__reduce_add_sync(0xffffffffu, cnt) >= Rc) ans = cand;
+        }
+        if (lane == 0) fl_l[0] = max(Lc, ans);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kStNW * 32) : "memory");
+      Lc = fl_l[0];
+    }
+    uint32_t* sl = a.slots + ((uint64_t)c * a.smax + seg) * kStSlotWords;
+    for (uint32_t e0 = 0; e0 < w.n; e0 += 32) {
+      const uint32_t e = e0 + lane;
+      const bool keep = e < w.n && w.keys[e] >= Lc;
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      uint32_t base = 0;
+      if (lane == 0 && bal) base = atomicAdd(&fl_ctr, __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (keep) {
+        const uint32_t d = base + __popc(bal & ((1u << lane) - 1u));
+        if (d < kStSlotCap) {
+          sl[2 + d] = w.keys[e];
+          sl[2 + kStSlotCap + d] = w.poss[e];
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kStNW * 32) : "memory");
+#ifdef ATKG_ST_DEBUG
+    if (threadIdx.x == 0 && c < 3) printf("cta %u seg %u ctr %u bad %u Lc %08x\n", c, seg, fl_ctr, fl_bad, Lc);
+    if (c < 2 && lane == 0) printf("cta %u seg %u warp %d n %u tkey %08x bad %u r %u\n", c, seg, warp, w.n, w.tkey, w.bad, w.r);
+#endif
+    if (threadIdx.x == 0) {
+      sl[0] = (fl_bad || fl_ctr > kStSlotCap) ? kStBadCount : fl_ctr;
+      sl[1] = Lc;
+      fl_ctr = 0;
+      fl_bad = 0;
+    }
   };
   uint32_t row = ~0u;
   auto process = [&](const Step& st, const uint4* sl) {
@@ -367,6 +435,7 @@ __global__ void __launch_bounds__(kStNW * 32, 2) st_stream_kernel(StArgs a) {
       w.tkey = 0;
       w.L = -INFINITY;
       const uint32_t seg = min(plen, st.row_end) - st.cur;  // vectors of this row in the piece
+      seg_len_e = seg * VE;
       const float share = (float)seg * (float)VE / (float)kStNW;
       w.r = (uint32_t)fminf(96.f, fmaxf(16.f, 8.f + ceilf(a.rfac * share)));
     }
@@ -566,6 +635,7 @@ struct StFinArgs {
   uint32_t G, smax, B, k;
   uint32_t ecap;   // gathered-entry capacity (shared memory)
   uint32_t force_slow;  // tests: every row takes the exact fallback
+  uint32_t* gate;       // giant rows: no in-kernel fallback, flag the row for the host instead
   const uint32_t* slots;
   float* out_v;
   uint32_t* out_i;
@@ -580,6 +650,7 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
   extern __shared__ __align__(128) uint8_t st_smem[];
   uint8_t* smem = st_smem;
   __shared__ uint32_t sh_l, sh_ne, sh_nk, sh_bad, sh_nc, sh_m;
+  __shared__ uint32_t pfx[kStMaxRowPieces + 1];
   __shared__ uint64_t red64[16];
   const uint32_t t = threadIdx.x, nt = blockDim.x;
   const uint64_t row = blockIdx.x;
@@ -603,62 +674,86 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
   const uint64_t va = row * nvrow, vb = (row + 1) * nvrow - 1;
   const uint32_t ca = (uint32_t)(va / a.psz), cb = (uint32_t)(vb / a.psz);
   const uint32_t seg_a = (uint32_t)(row - (uint64_t)ca * a.psz / nvrow);
-  const uint32_t nslots = (cb - ca + 1) * kStNW;
+  const uint32_t nslots = cb - ca + 1;
   auto slot_ptr = [&](uint32_t q) {
-    const uint32_t c = ca + q / kStNW, w = q % kStNW;
-    return a.slots + (((uint64_t)c * a.smax + (c == ca ? seg_a : 0u)) * kStNW + w) * kStSlotWords;
+    return a.slots + ((uint64_t)(ca + q) * a.smax + (q == 0 ? seg_a : 0u)) * kStSlotWords;
   };
   __syncthreads();  // counters initialised
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the stream kernel's slots are complete
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  // gather every slot's entries (one warp per slot; header and the first 64
-  // entries in one round trip), the row threshold L = max of slot thresholds
-  const int lane = t & 31, wq = t >> 5;
-  uint32_t lmax = 0;
-  for (uint32_t q = wq; q < nslots; q += nt / 32) {
-    const uint32_t* sl = slot_ptr(q);
-    const uint32_t hdr = lane < 2 ? sl[lane] : 0u;
-    uint32_t kk[2], pp[2];
+  // slot headers -> L = max of the slot thresholds (every element >= L is in
+  // some slot), entry counts -> prefix pfx[]
+  const int lane = t & 31;
+  {
+    uint32_t lmax = 0;
+    const uint32_t per = (nslots + nt - 1) / nt;
+    const uint32_t q0 = min(nslots, t * per), q1 = min(nslots, q0 + per);
+    uint32_t sum = 0;
+    for (uint32_t q = q0; q < q1; ++q) {
+      const uint32_t* sl = slot_ptr(q);
+      const uint32_t m = sl[0];
+      lmax = max(lmax, sl[1]);
+      if (m > kStSlotCap) sh_bad = 1u;
+#ifdef ATKG_ST_DEBUG
+      if (row < 3) printf("row %llu slot %u (piece %u) m %u L %08x\n", (unsigned long long)row, q, ca + q, m, sl[1]);
+#endif
+      pfx[q] = m > kStSlotCap ? 0u : m;
+      sum += m > kStSlotCap ? 0u : m;
+    }
+    lmax = __reduce_max_sync(0xffffffffu, lmax);
+    if (lane == 0 && lmax) atomicMax(&sh_l, lmax);
+    uint64_t tot;
+    uint32_t ex = (uint32_t)block_excl_scan64(sum, red64, &tot);
+    for (uint32_t q = q0; q < q1; ++q) {
+      const uint32_t m = pfx[q];
+      pfx[q] = ex;
+      ex += m;
+    }
+    if (t == 0) pfx[nslots] = (uint32_t)tot;
+  }
+  __syncthreads();
+  const uint32_t Lk = sh_l, E = pfx[nslots];
+  // every entry >= L, flattened over the slots (binary search for the slot);
+  // four entries per thread per trip so their loads overlap
+  auto slot_of = [&](uint32_t e) {  // pfx[lo] <= e < pfx[lo + 1]
+    uint32_t lo = 0, hi = nslots;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (pfx[mid] <= e) lo = mid;
+      else hi = mid;
+    }
+    return lo;
+  };
+  for (uint32_t e0 = 0; e0 < E; e0 += 4 * nt) {
+    uint32_t key[4], q[4];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      kk[h] = sl[2 + h * 32 + lane];
-      pp[h] = sl[2 + kStSlotCap + h * 32 + lane];
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t e = e0 + u * nt + t;
+      q[u] = e < E ? slot_of(e) : 0u;
+      key[u] = e < E ? slot_ptr(q[u])[2 + (e - pfx[q[u]])] : 0u;
     }
-    const uint32_t m = __shfl_sync(0xffffffffu, hdr, 0);
-    lmax = max(lmax, __shfl_sync(0xffffffffu, hdr, 1));
-    if (m > kStSlotCap) {
-      if (lane == 0) sh_bad = 1u;
-      continue;
-    }
-    uint32_t base = 0;
-    if (lane == 0 && m) base = atomicAdd(&sh_ne, m);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    for (uint32_t e0 = 0; e0 < m; e0 += 32) {
-      const uint32_t e = e0 + lane;
-      uint32_t key, pos;
-      if (e0 < 64) {
-        key = e0 == 0 ? kk[0] : kk[1];
-        pos = e0 == 0 ? pp[0] : pp[1];
-      } else {
-        key = e < m ? sl[2 + e] : 0u;
-        pos = e < m ? sl[2 + kStSlotCap + e] : 0u;
-      }
-      if (e < m && base + e < a.ecap) {
-        ek[base + e] = key;
-        ep[base + e] = pos;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t e = e0 + u * nt + t;
+      if (e < E && key[u] >= Lk) {
+        const uint32_t d = atomicAdd(&sh_ne, 1u);
+        if (d < a.ecap) {
+          const uint32_t pos = slot_ptr(q[u])[2 + kStSlotCap + (e - pfx[q[u]])];
+          ek[d] = key[u];
+          ep[d] = pos;
+          atomicAdd(&cnt[bucket(pos)], 1u);
+        }
       }
     }
   }
-  if (lmax) atomicMax(&sh_l, lmax);
   __syncthreads();
-  const uint32_t Lk = sh_l, ne_all = sh_ne;
+  const uint32_t ne_all = sh_ne;
   bool fast = sh_bad == 0 && Lk > kStKeyNegInf && !a.force_slow && ne_all <= a.ecap;
+#ifdef ATKG_ST_DEBUG
+  if (t == 0 && row < 3) printf("row %llu nslots %u ca %u cb %u seg_a %u bad %u Lk %08x E %u ne %u\n", (unsigned long long)row, nslots, ca, cb, seg_a, sh_bad, Lk, E, ne_all);
+#endif
   if (fast) {
-    uint32_t nk = 0;
-    for (uint32_t q = t; q < ne_all; q += nt)
-      if (ek[q] >= Lk) { atomicAdd(&cnt[bucket(ep[q])], 1u); ++nk; }
-    nk = __reduce_add_sync(0xffffffffu, nk);
-    if (lane == 0 && nk) atomicAdd(&sh_nk, nk);
+    if (t == 0) sh_nk = ne_all;
     __syncthreads();
     const uint32_t ne = sh_nk;
     {
@@ -674,7 +769,6 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
       if (t == 0) sh_m = (uint32_t)(tot >> 32);
       __syncthreads();
       for (uint32_t q = t; q < ne_all; q += nt) {
-        if (ek[q] < Lk) continue;
         const uint32_t d = atomicAdd(&cur[bucket(ep[q])], 1u);
         gk[d] = ek[q];
         gp[d] = ep[q];
@@ -718,6 +812,13 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
   }
   __syncthreads();
   uint32_t M = sh_nc;
+#ifdef ATKG_ST_DEBUG
+  if (t == 0 && row < 3) printf("row %llu fast %d M %u m %u\n", (unsigned long long)row, (int)fast, M, sh_m);
+#endif
+  if (!fast && a.gate) {  // giant row: the host reruns the exact path
+    if (t == 0) atomicOr(a.gate, 1u);
+    return;
+  }
   if (!fast) {
     // exact fallback: Alg. 1 summaries of every bucket over the whole row
     const T* x = static_cast<const T*>(a.in) + row * a.n;

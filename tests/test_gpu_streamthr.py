@@ -139,3 +139,18 @@ def test_streamthr_matches_previous_path(cuda):
     finally:
         del os.environ["ATKG_NO_STREAMTHR"]
     assert np.array_equal(bits(v), bits(v2)) and np.array_equal(u32(i), u32(i2))
+
+
+@pytest.mark.parametrize("force", [False, True])
+def test_streamthr_giant_row_gate(cuda, ref, monkeypatch, force):
+    """Giant-row mode (no in-kernel fallback): a failed row is flagged and the
+    host reruns the exact path; both outcomes match the reference."""
+    monkeypatch.setenv("ATKG_ST_GIANT_N", "65536")
+    if force:
+        monkeypatch.setenv("ATKG_ST_FORCE_SLOW", "1")
+    rng = np.random.default_rng(77)
+    x = rng.standard_normal((2, 1 << 21)).astype(np.float32)
+    check(ref, cuda, x, "f32", 256, 8, 1024)
+    x = rng.standard_normal((3, 262144)).astype(np.float32)
+    x[1] = np.arange(262144, dtype=np.float32)  # ramp: the threshold fails
+    check(ref, cuda, x, "f32", 128, 2, 64)
