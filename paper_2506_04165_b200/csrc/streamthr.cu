@@ -99,17 +99,28 @@ StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint
   sp.G = (uint32_t)((sp.vtot + sp.psz - 1) / sp.psz);
   // rows spanned by any piece
   const uint64_t nvrow = n / ve;
-  uint64_t smax = 1;
-  for (uint32_t c = 0; c < sp.G; ++c) {
-    const uint64_t v0 = st_piece_start(sp.vtot, sp.psz, c), v1 = st_piece_start(sp.vtot, sp.psz, c + 1);
-    if (v1 > v0) smax = std::max<uint64_t>(smax, (v1 - 1) / nvrow - v0 / nvrow + 1);
+  // (memoised: the planner runs on every call)
+  thread_local uint64_t m_vtot = 0, m_psz = 0, m_nvrow = 0, m_smax = 1;
+  if (m_vtot != sp.vtot || m_psz != sp.psz || m_nvrow != nvrow) {
+    uint64_t smax = 1;
+    for (uint32_t c = 0; c < sp.G; ++c) {
+      const uint64_t v0 = st_piece_start(sp.vtot, sp.psz, c), v1 = st_piece_start(sp.vtot, sp.psz, c + 1);
+      if (v1 > v0) smax = std::max<uint64_t>(smax, (v1 - 1) / nvrow - v0 / nvrow + 1);
+    }
+    m_vtot = sp.vtot; m_psz = sp.psz; m_nvrow = nvrow; m_smax = smax;
   }
-  sp.smax = (uint32_t)smax;
+  sp.smax = (uint32_t)m_smax;
   // target count T of row elements >= L: B * E[min(K', Poisson(T/B))] must
   // clear K with margin; every warp sub-stream keeps ~2x its share of T
   const double need = 1.2 * k + 4.0 * std::sqrt((double)k) + 8.0;
-  double T = 1.0;
-  while (T < (double)n && (double)B * mean_min_poisson(T / (double)B, kp) < need) T *= 1.05;
+  thread_local uint64_t t_n = 0, t_B = 0, t_kp = 0, t_k = 0;
+  thread_local double t_T = 1.0;
+  if (t_n != n || t_B != B || t_kp != kp || t_k != k) {
+    double T0 = 1.0;
+    while (T0 < (double)n && (double)B * mean_min_poisson(T0 / (double)B, kp) < need) T0 *= 1.05;
+    t_n = n; t_B = B; t_kp = kp; t_k = k; t_T = T0;
+  }
+  const double T = t_T;
   sp.rfac = (float)(2.0 * T / (double)n);
   sp.lfac = (float)(T / 1.5 / (double)n);
   // rows cut into many pieces (the giant row): cap each slot at ~3x its share

@@ -45,12 +45,19 @@
 namespace atkg {
 
 constexpr int kStNW = 8;           // consumer warps per CTA
-constexpr uint32_t kStLog = 256;   // log entries per warp
+#ifndef ATKG_ST_LOG
+#define ATKG_ST_LOG 256
+#endif
+#ifndef ATKG_ST_SLOTS
+#define ATKG_ST_SLOTS 2
+#endif
+constexpr uint32_t kStLog = ATKG_ST_LOG;   // log entries per warp
 constexpr uint32_t kStWarpCap = 128;  // entries a warp keeps at a flush
 constexpr uint32_t kStSlotCap = 1024;  // entries per (piece, row segment) slot
 constexpr uint32_t kStSlotWords = 2 + 2 * kStSlotCap;  // {count, Lkey} | keys | positions
 constexpr uint32_t kStBadCount = 0xffffffffu;
 constexpr uint32_t kStMaxRowPieces = 2048;  // pieces one row may span (host-checked)
+constexpr uint32_t kStFewSlots = 3;         // finish: one-round-trip gather up to this many slots
 
 // ascending order key of a non-NaN float, -0 == +0
 __device__ __forceinline__ uint32_t st_okey(float x) {
@@ -291,7 +298,7 @@ __device__ __forceinline__ uint32_t st_warp_rth16(const uint32_t (&k)[N], uint32
 // eighth of every step and streams it through its own kStSlots-deep ring of
 // shared-memory slots with 1-D TMA bulk copies (no cross-warp hand-off: the
 // warp refills a slot as soon as it has read it).
-constexpr int kStSlots = 2;
+constexpr int kStSlots = ATKG_ST_SLOTS;
 
 template <typename T, int UNR>
 __global__ void __launch_bounds__(kStNW * 32, 2) st_stream_kernel(StArgs a) {
@@ -684,7 +691,69 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
   // slot headers -> L = max of the slot thresholds (every element >= L is in
   // some slot), entry counts -> prefix pfx[]
   const int lane = t & 31;
-  {
+  uint32_t Lk;
+  if (nslots <= kStFewSlots && a.ecap >= 1024) {
+    // few slots (rows over a handful of pieces): every thread reads the
+    // headers (broadcast) and, speculatively, its share of every slot's
+    // entries in the same round trip; filter against L = max threshold
+    constexpr uint32_t PER = kStSlotCap / 256;
+    uint32_t kk[kStFewSlots][PER], pp[kStFewSlots][PER], mq[kStFewSlots];
+    Lk = 0;
+    bool bad = false;
+#pragma unroll
+    for (uint32_t q = 0; q < kStFewSlots; ++q) {
+      if (q < nslots) {
+        const uint32_t* sl = slot_ptr(q);
+        mq[q] = sl[0];
+        Lk = max(Lk, sl[1]);
+        bad |= mq[q] > kStSlotCap;
+#pragma unroll
+        for (uint32_t i = 0; i < PER; ++i) {
+          kk[q][i] = sl[2 + i * 256 + (t & 255)];
+          pp[q][i] = sl[2 + kStSlotCap + i * 256 + (t & 255)];
+        }
+      } else {
+        mq[q] = 0;
+      }
+    }
+    if (t == 0) { sh_l = Lk; if (bad) sh_bad = 1u; }
+    if (!bad && nt == 256) {
+#pragma unroll
+      for (uint32_t q = 0; q < kStFewSlots; ++q) {
+#pragma unroll
+        for (uint32_t i = 0; i < PER; ++i) {
+          const uint32_t e = i * 256 + t;
+          if (e < mq[q] && kk[q][i] >= Lk) {
+            const uint32_t d = atomicAdd(&sh_ne, 1u);
+            if (d < a.ecap) {
+              ek[d] = kk[q][i];
+              ep[d] = pp[q][i];
+              atomicAdd(&cnt[bucket(pp[q][i])], 1u);
+            }
+          }
+        }
+      }
+    }
+  } else {
+  if (nslots <= 32) {  // one warp: headers, max, prefix by shuffles
+    if (t < 32) {
+      const uint32_t* sl = lane < (int)nslots ? slot_ptr(lane) : nullptr;
+      const uint32_t m0 = sl ? sl[0] : 0u, l0 = sl ? sl[1] : 0u;
+      const bool bad = m0 > kStSlotCap;
+      const uint32_t m = bad ? 0u : m0;
+      uint32_t incl = m;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane < (int)nslots) pfx[lane] = incl - m;
+      if (lane == (int)nslots - 1) pfx[nslots] = incl;
+      const uint32_t lmax = __reduce_max_sync(0xffffffffu, l0);
+      if (__any_sync(0xffffffffu, bad) && lane == 0) sh_bad = 1u;
+      if (lane == 0) sh_l = lmax;
+    }
+  } else {
     uint32_t lmax = 0;
     const uint32_t per = (nslots + nt - 1) / nt;
     const uint32_t q0 = min(nslots, t * per), q1 = min(nslots, q0 + per);
@@ -694,9 +763,6 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
       const uint32_t m = sl[0];
       lmax = max(lmax, sl[1]);
       if (m > kStSlotCap) sh_bad = 1u;
-#ifdef ATKG_ST_DEBUG
-      if (row < 3) printf("row %llu slot %u (piece %u) m %u L %08x\n", (unsigned long long)row, q, ca + q, m, sl[1]);
-#endif
       pfx[q] = m > kStSlotCap ? 0u : m;
       sum += m > kStSlotCap ? 0u : m;
     }
@@ -712,7 +778,8 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
     if (t == 0) pfx[nslots] = (uint32_t)tot;
   }
   __syncthreads();
-  const uint32_t Lk = sh_l, E = pfx[nslots];
+  Lk = sh_l;
+  const uint32_t E = pfx[nslots];
   // every entry >= L, flattened over the slots (binary search for the slot);
   // four entries per thread per trip so their loads overlap
   auto slot_of = [&](uint32_t e) {  // pfx[lo] <= e < pfx[lo + 1]
@@ -746,6 +813,7 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
       }
     }
   }
+  }
   __syncthreads();
   const uint32_t ne_all = sh_ne;
   bool fast = sh_bad == 0 && Lk > kStKeyNegInf && !a.force_slow && ne_all <= a.ecap;
@@ -753,9 +821,7 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
   if (t == 0 && row < 3) printf("row %llu nslots %u ca %u cb %u seg_a %u bad %u Lk %08x E %u ne %u\n", (unsigned long long)row, nslots, ca, cb, seg_a, sh_bad, Lk, E, ne_all);
 #endif
   if (fast) {
-    if (t == 0) sh_nk = ne_all;
-    __syncthreads();
-    const uint32_t ne = sh_nk;
+    const uint32_t ne = ne_all;
     {
       // M and bucket offsets (block scan over buckets; thread owns a run)
       const uint32_t per = (B + nt - 1) / nt;
@@ -839,16 +905,16 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
     if (nan) atomicOr(a.status, ATKG_FLAG_NAN);
     M = B * filled;
   }
-  uint32_t P = 2;
-  while (P < M) P <<= 1;
-  for (uint32_t q = M + t; q < P; q += nt) cand[q] = ~0ull;
-  __syncthreads();
   if (fast) {
     // unique keys (real elements >= L > -inf): counting sort on the key's
     // value word (ascending = value descending), ranks inside a bin by
     // comparison; the first k ranks are the output
     if (st_emit_ranked(cand, gk, M, a.k, a.out_v + row * a.k, a.out_i + row * a.k)) return;
   }
+  uint32_t P = 2;
+  while (P < M) P <<= 1;
+  for (uint32_t q = M + t; q < P; q += nt) cand[q] = ~0ull;
+  __syncthreads();
   group_bitonic_sort<uint64_t>(cand, P, t, nt);
   for (uint32_t q = t; q < a.k; q += nt) {
     const uint64_t key = cand[q];
