@@ -479,6 +479,7 @@ uint64_t select_ws_bytes(uint64_t rows, uint64_t count, uint32_t k) {
 void run_select(const float* vals, const uint32_t* idx, uint64_t rows, uint64_t count, uint64_t stride, uint32_t k,
                 uint64_t limit, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st) {
   const uint32_t P = next_pow2(count);
+  if (run_select_ranked(vals, idx, rows, count, stride, k, limit, ov, oi, status, st)) return;
   if (P <= 512) {  // one warp per row, keys in registers
     const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
     const uint32_t c32 = static_cast<uint32_t>(count);

@@ -79,6 +79,11 @@ PipePlan plan_rowpipe(int dtype, const void* in, uint64_t rows, uint64_t n, uint
 void run_rowpipe(const PipePlan& pp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
                  float* ov, uint32_t* oi, uint32_t* status, cudaStream_t st);
 
+// stage 2 by counting-sort ranks for 128 < count <= 1024 (streamthr.cu);
+// false if not applicable
+bool run_select_ranked(const float* vals, const uint32_t* idx, uint64_t rows, uint64_t count, uint64_t stride,
+                       uint32_t k, uint64_t limit, float* ov, uint32_t* oi, uint32_t* status, cudaStream_t st);
+
 // threshold-stream approx_top_k for long rows (streamthr.cu)
 struct StPlan {
   bool ok = false, giant = false;

@@ -199,4 +199,15 @@ void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, u
 #undef ATKG_ST_FIN
 }
 
+bool run_select_ranked(const float* vals, const uint32_t* idx, uint64_t rows, uint64_t count, uint64_t stride,
+                       uint32_t k, uint64_t limit, float* ov, uint32_t* oi, uint32_t* status, cudaStream_t st) {
+  if (env_u64("ATKG_NO_RANK_SELECT", 0) || count <= 128 || count > 1024) return false;
+  uint32_t P = 2;
+  while (P < count) P <<= 1;
+  stage2_rank_kernel<<<(unsigned)rows, 128, (size_t)P * 16, st>>>(vals, idx, (uint32_t)count, stride, k, limit, P,
+                                                                     ov, oi, status);
+  check_launch();
+  return true;
+}
+
 }  // namespace atkg

@@ -636,6 +636,54 @@ __device__ __forceinline__ bool st_emit_ranked(const uint64_t* keys, uint32_t* m
   return true;
 }
 
+
+// Stage 2 (select_top_k_candidates, topk.cpp:192-236) for 128 < count <=
+// 1024 candidates per row: one CTA of 128 threads per row, survivors
+// (index < limit) compacted into shared memory, then the counting-sort rank
+// emit; rows holding -inf (sentinel keys may repeat) or crowded bins sort
+// with a bitonic network instead.  smem: keys[P] | mem[P] (u64).
+__global__ void __launch_bounds__(128) stage2_rank_kernel(const float* __restrict__ vals,
+                                                          const uint32_t* __restrict__ idx, uint32_t count,
+                                                          uint64_t stride, uint32_t k, uint64_t index_limit,
+                                                          uint32_t P, float* out_v, uint32_t* out_i,
+                                                          uint32_t* status) {
+  extern __shared__ __align__(16) uint64_t s2_keys[];
+  __shared__ uint32_t nsurv, flags;
+  uint64_t* keys = s2_keys;
+  uint32_t* mem32 = reinterpret_cast<uint32_t*>(s2_keys + P);
+  const uint64_t row = blockIdx.x;
+  const uint32_t t = threadIdx.x;
+  if (t == 0) { nsurv = 0; flags = 0; }
+  __syncthreads();
+  uint32_t f = 0;
+  for (uint32_t c = t; c < count; c += blockDim.x) {
+    const float v = vals[row * stride + c];
+    const uint32_t ix = idx[row * stride + c];
+    if (v != v) f |= 1u;
+    if (v == -INFINITY) f |= 2u;
+    if ((uint64_t)ix < index_limit) keys[atomicAdd(&nsurv, 1u)] = rank_key_bits(__float_as_uint(v), ix);
+  }
+  if (f) atomicOr(&flags, f);
+  __syncthreads();
+  const uint32_t M = nsurv;
+  if (flags & 1u) {
+    if (t == 0) atomicOr(status, ATKG_FLAG_NAN);
+    return;
+  }
+  if (M < k) {
+    if (t == 0) atomicOr(status, kFlagFew);
+    return;
+  }
+  if (!(flags & 2u) && st_emit_ranked(keys, mem32, M, k, out_v + row * k, out_i + row * k)) return;
+  for (uint32_t q = M + t; q < P; q += blockDim.x) keys[q] = ~0ull;
+  __syncthreads();
+  block_bitonic_sort(keys, P);
+  for (uint32_t q = t; q < k; q += blockDim.x) {
+    out_v[row * k + q] = __uint_as_float(key_value_bits(keys[q]));
+    out_i[row * k + q] = (uint32_t)keys[q];
+  }
+}
+
 struct StFinArgs {
   const void* in;
   uint64_t n, vtot, psz;

@@ -300,3 +300,34 @@ def test_rowres_ties_vs_reference(cuda, ref, levels, B, kp, k):
     rg = [ref.stage1(f[r], B, kp) for r in range(4)]
     for r in range(4):
         assert np.array_equal(bits(gv[r]), bits(rg[r][0])) and np.array_equal(u32(gi[r]), rg[r][1])
+
+
+@pytest.mark.parametrize("count", [129, 300, 512, 700, 1024])
+def test_select_candidates_rank_path_vs_port(cuda, port, count):
+    """Stage 2 through the counting-sort rank kernel (128 < count <= 1024):
+    ties, -0.0, -inf sentinels, index_limit drops, quantised values."""
+    rng = np.random.default_rng(count)
+    cases = []
+    v = rng.standard_normal(count).astype(np.float32)
+    cases.append((v, rng.permutation(count).astype(np.uint32)))
+    v = rng.integers(-3, 4, count).astype(np.float32)
+    v[rng.integers(0, count, count // 8)] = -0.0
+    cases.append((v, rng.permutation(count).astype(np.uint32)))
+    v = rng.standard_normal(count).astype(np.float32)
+    v[: count // 3] = -np.inf
+    i = rng.permutation(count).astype(np.uint32)
+    i[: count // 3] = 0  # duplicate sentinel keys {-inf, 0}
+    cases.append((v, i))
+    v = (rng.standard_normal(count) * np.float32(1e30) ** rng.random(count)).astype(np.float32)
+    cases.append((v, rng.permutation(count).astype(np.uint32)))
+    for v, i in cases:
+        for k in (1, min(count, 64), min(count, 287), count):
+            for lim in (2**64 - 1, int(count * 0.9)):
+                try:
+                    pv, pi = port.select_candidates(v, i, k, lim)
+                except ValueError:
+                    with pytest.raises(ValueError):
+                        atk.select_top_k_candidates(v, i, k, lim)
+                    continue
+                r = atk.select_top_k_candidates(v, i, k, lim)
+                assert np.array_equal(bits(r.values), bits(pv)) and np.array_equal(r.indices, pi)
