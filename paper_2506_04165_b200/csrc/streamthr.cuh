@@ -38,6 +38,7 @@
 #include <cuda_bf16.h>
 
 #include "common.cuh"
+#include "emit.cuh"
 #include "ptx.cuh"
 #include "rowthr.cuh"
 #include "summ.cuh"
@@ -566,76 +567,14 @@ __global__ void __launch_bounds__(kStNW * 32, 2) st_stream_kernel(StArgs a) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Emits the first k (ascending) of M unique 64-bit keys: bins on the high
-// word (ascending with the key), a counting sort into `mem` (M u64, 8-byte
-// aligned), ranks inside a bin by comparison.  Block-wide; returns false
-// (nothing written) when a bin is too crowded -- the caller sorts instead.
+// first k of M unique 64-bit rank keys (emit.cuh); false: bins too crowded
 __device__ __forceinline__ bool st_emit_ranked(const uint64_t* keys, uint32_t* mem32, uint32_t M, uint32_t k,
                                                float* ov, uint32_t* oi) {
-  constexpr uint32_t NB = 256, RUN = 48;
-  __shared__ uint32_t hlo, hhi, hist[NB + 1], curs[NB], hmax;
-  uint64_t* mem = reinterpret_cast<uint64_t*>(mem32);
-  const uint32_t t = threadIdx.x, nt = blockDim.x;
-  if (t == 0) { hlo = 0xffffffffu; hhi = 0; hmax = 0; }
-  for (uint32_t b = t; b <= NB; b += nt) hist[b] = 0;
-  __syncthreads();
-  uint32_t lo = 0xffffffffu, hi = 0;
-  for (uint32_t q = t; q < M; q += nt) {
-    const uint32_t h = (uint32_t)(keys[q] >> 32);
-    lo = min(lo, h);
-    hi = max(hi, h);
-  }
-  lo = __reduce_min_sync(0xffffffffu, lo);
-  hi = __reduce_max_sync(0xffffffffu, hi);
-  if ((t & 31) == 0) { atomicMin(&hlo, lo); atomicMax(&hhi, hi); }
-  __syncthreads();
-  lo = hlo;
-  const uint32_t span = hhi - lo;
-  const uint32_t shift = span < NB ? 0u : (uint32_t)(32 - __clz((int)(span >> 8)));  // span >> shift < NB
-  auto bin = [&](uint64_t key) { return ((uint32_t)(key >> 32) - lo) >> shift; };
-  for (uint32_t q = t; q < M; q += nt) atomicAdd(&hist[bin(keys[q])], 1u);
-  __syncthreads();
-  if (t < 32) {  // exclusive scan of NB bins, 8 per lane
-    uint32_t c[NB / 32], tot = 0, mx = 0;
-#pragma unroll
-    for (int i = 0; i < (int)(NB / 32); ++i) { c[i] = hist[t * (NB / 32) + i]; tot += c[i]; mx = max(mx, c[i]); }
-    uint32_t incl = tot;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if ((int)t >= o) incl += y;
-    }
-    uint32_t ex = incl - tot;
-#pragma unroll
-    for (int i = 0; i < (int)(NB / 32); ++i) {
-      hist[t * (NB / 32) + i] = ex;
-      curs[t * (NB / 32) + i] = ex;
-      ex += c[i];
-    }
-    mx = __reduce_max_sync(0xffffffffu, mx);
-    if (t == 0) { hist[NB] = M; hmax = mx; }
-  }
-  __syncthreads();
-  if (hmax > RUN) return false;  // uniform
-  for (uint32_t q = t; q < M; q += nt) {
-    const uint64_t key = keys[q];
-    mem[atomicAdd(&curs[bin(key)], 1u)] = key;
-  }
-  __syncthreads();
-  for (uint32_t q = t; q < M; q += nt) {
-    const uint64_t key = mem[q];
-    const uint32_t b = bin(key);
-    const uint32_t b0 = hist[b], b1 = hist[b + 1];
-    uint32_t r = b0;
-    for (uint32_t o = b0; o < b1; ++o) r += mem[o] < key ? 1u : 0u;
-    if (r < k) {
-      ov[r] = __uint_as_float(key_value_bits(key));
-      oi[r] = (uint32_t)key;
-    }
-  }
-  return true;
+  return emit_ranked<uint64_t>(keys, reinterpret_cast<uint64_t*>(mem32), M, k, [&](uint32_t r, uint64_t key) {
+    ov[r] = __uint_as_float(key_value_bits(key));
+    oi[r] = (uint32_t)key;
+  });
 }
-
 
 // Stage 2 (select_top_k_candidates, topk.cpp:192-236) for 128 < count <=
 // 1024 candidates per row: one CTA of 128 threads per row, survivors
