@@ -690,7 +690,9 @@ def main():
     launches0 = lib.atkg_launch_count()
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
-        lib.atkg_profile_begin()
+        # dominant-kernel CUDA events on every 16th step only: a bracket sits
+        # between that kernel and its PDL-launched successor
+        lib.atkg_profile_begin_every(int(os.environ.get("ATKG_BENCH_PROF_EVERY", "16")))
         clocks.mark()
         ev0.record(stream)
         for _ in range(args.steps):

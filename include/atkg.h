@@ -242,6 +242,10 @@ void atkg_bf16_to_f32(const uint16_t* in, uint64_t count, float* out, uint32_t t
  * returns the summed device duration and the number of such launches.
  * Process-wide; not for concurrent use. */
 void atkg_profile_begin(void);
+/* Same, bracketing only every `every`-th dominant-kernel launch: the event
+ * records sit between a kernel and its PDL-launched successor, so sampling
+ * keeps the timed loop's step time unperturbed. */
+void atkg_profile_begin_every(uint32_t every);
 int atkg_profile_end(double* total_ms, uint64_t* launches);
 /* Kernels launched by this library so far (process-wide counter). */
 uint64_t atkg_launch_count(void);

@@ -86,6 +86,7 @@ def _load():
         "atkg_f32_to_bf16": ([vp, u64, vp, u32], None),
         "atkg_bf16_to_f32": ([vp, u64, vp, u32], None),
         "atkg_profile_begin": ([], None),
+        "atkg_profile_begin_every": ([C.c_uint32], None),
         "atkg_profile_end": ([f64p, C.POINTER(C.c_uint64)], i32),
         "atkg_launch_count": ([], u64),
     }

@@ -3,6 +3,9 @@
 // accumulator.  Kernels live in stage1.cuh / stage2.cuh / radix.cuh.
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
@@ -596,9 +599,14 @@ int atkg_set_device(int device) {
   return guarded([&] { CUDA_OK(cudaSetDevice(device)); });
 }
 
-void atkg_profile_begin(void) {
+void atkg_profile_begin(void) { atkg_profile_begin_every(1); }
+
+void atkg_profile_begin_every(uint32_t every) {
   g_prof.on = true;
   g_prof.used = 0;
+  g_prof.every = every ? every : 1;
+  g_prof.seen = 0;
+  g_prof.open = false;
 }
 
 int atkg_profile_end(double* total_ms, uint64_t* launches) {
@@ -637,7 +645,7 @@ int atkg_workspace_size(int op, int dtype, uint64_t rows, const atkg_params* p, 
                  select_ws_bytes(rows, filled_count(*p), p->global_k);
         const ThrPlan tp = plan_rowthr(dtype, aligned, p->n, p->num_buckets, p->local_k, p->global_k);
         if (tp.ok) *bytes = std::max<size_t>(*bytes, rowthr_ws_bytes(rows, tp));
-        const StPlan sp = plan_streamthr(dtype, aligned, rows, p->n, p->num_buckets, p->local_k, p->global_k);
+        const StPlan sp = plan_streamthr(dtype, aligned, rows, p->n, p->num_buckets, p->local_k, p->global_k, true);
         if (sp.ok) *bytes = std::max<size_t>(*bytes, sp.ws_bytes);
         break;
       }
@@ -694,6 +702,33 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     if (rows == 0) return;
     (void)ws_bytes;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+#ifdef ATKG_HOST_PROF
+    static double acc[3] = {0, 0, 0};
+    static long calls = 0;
+    auto t0 = std::chrono::steady_clock::now();
+#endif
+    const StPlan sp = plan_streamthr(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
+#ifdef ATKG_HOST_PROF
+    auto t1 = std::chrono::steady_clock::now();
+#endif
+    if (sp.ok) {  // long rows: threshold stream + per-row finish (exact fallback per row)
+      void* sws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(d_ws)));
+      run_streamthr(dtype, sp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,
+                    sws, d_status, st);
+#ifdef ATKG_HOST_PROF
+      auto t2 = std::chrono::steady_clock::now();
+      acc[0] += std::chrono::duration<double, std::micro>(t1 - t0).count();
+      acc[1] += std::chrono::duration<double, std::micro>(t2 - t1).count();
+      if (++calls % 1000 == 0) fprintf(stderr, "host: plan %.2f us, launches %.2f us per call\n", acc[0] / calls, acc[1] / calls);
+#endif
+      if (!sp.giant) return;
+      // giant rows: read the gate (4 bytes) and rerun the exact path if a
+      // row's threshold failed (the device cannot afford that fallback)
+      uint32_t gate = 0;
+      CUDA_OK(cudaMemcpyAsync(&gate, static_cast<char*>(sws) + (sp.ws_bytes - 256), 4, cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaStreamSynchronize(st));
+      if (!gate) return;
+    }
     const S1Plan pl = plan_stage1(dtype, d_in, rows, p->n, p->n, p->num_buckets, p->local_k);
     char* w = static_cast<char*>(d_ws);
     w = reinterpret_cast<char*>(align_up(reinterpret_cast<uintptr_t>(w)));
@@ -703,19 +738,6 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     float* gv = reinterpret_cast<float*>(w);
     uint32_t* gi = reinterpret_cast<uint32_t*>(w + rows * gstride * 4);
     w += grid_bytes(rows, *p);
-    const StPlan sp = plan_streamthr(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
-    if (sp.ok) {  // long rows: threshold stream + per-row finish (exact fallback per row)
-      void* sws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(d_ws)));
-      run_streamthr(dtype, sp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,
-                    sws, d_status, st);
-      if (!sp.giant) return;
-      // giant rows: read the gate (4 bytes) and rerun the exact path if a
-      // row's threshold failed (the device cannot afford that fallback)
-      uint32_t gate = 0;
-      CUDA_OK(cudaMemcpyAsync(&gate, static_cast<char*>(sws) + (sp.ws_bytes - 256), 4, cudaMemcpyDeviceToHost, st));
-      CUDA_OK(cudaStreamSynchronize(st));
-      if (!gate) return;
-    }
     const PipePlan pp = plan_rowpipe(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
     if (pp.ok) {  // bf16 rows in shared memory: persistent row pipeline, row threshold
       run_rowpipe(pp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx, d_status, st);

@@ -26,8 +26,12 @@ struct Profiler {
   bool on = false;
   std::vector<cudaEvent_t> ev;  // pairs
   size_t used = 0;
+  uint32_t every = 1, seen = 0;  // bracket every `every`-th launch
+  bool open = false;
   void bracket_begin(cudaStream_t st) {
     if (!on) return;
+    open = (seen++ % every) == 0;
+    if (!open) return;
     if (used + 2 > ev.size()) {
       for (int q = 0; q < 2; ++q) {
         cudaEvent_t e;
@@ -38,7 +42,8 @@ struct Profiler {
     CUDA_OK(cudaEventRecord(ev[used], st));
   }
   void bracket_end(cudaStream_t st) {
-    if (!on) return;
+    if (!on || !open) return;
+    open = false;
     CUDA_OK(cudaEventRecord(ev[used + 1], st));
     used += 2;
   }
@@ -92,7 +97,9 @@ struct StPlan {
   float rfac = 0.f, lfac = 0.f, cfac = 0.f;
   size_t smem_stream = 0, smem_fin = 0;
 };
-StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k);
+// for_size: ignore the ATKG_NO_STREAMTHR switch (workspace sizing covers every path)
+StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
+                      bool for_size = false);
 void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
                    uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
 

@@ -72,9 +72,10 @@ void launch_finish(const StPlan& sp, uint64_t rows, const StFinArgs& a, cudaStre
 
 }  // namespace
 
-StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k) {
+StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
+                      bool for_size) {
   StPlan sp;
-  if (env_u64("ATKG_NO_STREAMTHR", 0)) return sp;
+  if (!for_size && env_u64("ATKG_NO_STREAMTHR", 0)) return sp;
   if (kp != 1 && kp != 2 && kp != 4 && kp != 8) return sp;
   const uint64_t es = dtype == ATKG_BF16 ? 2 : 4;
   const uint64_t ve = 16 / es;

@@ -1,0 +1,10 @@
+mkdir -p gpurun_out/r01e
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/r01e/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/r01e/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r01e/smoke.log 2>&1; echo rc=$? >> gpurun_out/r01e/smoke.log
+timeout 600 python bench.py > gpurun_out/r01e/bench_C2.json 2> gpurun_out/r01e/bench_C2.err
+timeout 600 python bench.py --config C3 > gpurun_out/r01e/bench_C3.json 2> gpurun_out/r01e/bench_C3.err
+timeout 900 python bench.py --config C4 > gpurun_out/r01e/bench_C4.json 2> gpurun_out/r01e/bench_C4.err
+timeout 900 python bench.py --config C5 > gpurun_out/r01e/bench_C5.json 2> gpurun_out/r01e/bench_C5.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r01e/bench_ref_C2.json 2> gpurun_out/r01e/bench_ref.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/r01e/launches_C2.csv python bench.py --config C2 --steps 20 --warmup 3 --no-cpu --e2e-steps 1 > /dev/null 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/r01e/launches_C4.csv python bench.py --config C4 --steps 5 --warmup 3 --no-cpu --e2e-steps 1 > /dev/null 2>&1
