@@ -3,9 +3,6 @@
 // accumulator.  Kernels live in stage1.cuh / stage2.cuh / radix.cuh.
 #include <cuda_runtime.h>
 
-#include <chrono>
-#include <cstdio>
-
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
@@ -702,25 +699,11 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     if (rows == 0) return;
     (void)ws_bytes;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-#ifdef ATKG_HOST_PROF
-    static double acc[3] = {0, 0, 0};
-    static long calls = 0;
-    auto t0 = std::chrono::steady_clock::now();
-#endif
     const StPlan sp = plan_streamthr(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
-#ifdef ATKG_HOST_PROF
-    auto t1 = std::chrono::steady_clock::now();
-#endif
     if (sp.ok) {  // long rows: threshold stream + per-row finish (exact fallback per row)
       void* sws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(d_ws)));
       run_streamthr(dtype, sp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,
                     sws, d_status, st);
-#ifdef ATKG_HOST_PROF
-      auto t2 = std::chrono::steady_clock::now();
-      acc[0] += std::chrono::duration<double, std::micro>(t1 - t0).count();
-      acc[1] += std::chrono::duration<double, std::micro>(t2 - t1).count();
-      if (++calls % 1000 == 0) fprintf(stderr, "host: plan %.2f us, launches %.2f us per call\n", acc[0] / calls, acc[1] / calls);
-#endif
       if (!sp.giant) return;
       // giant rows: read the gate (4 bytes) and rerun the exact path if a
       // row's threshold failed (the device cannot afford that fallback)

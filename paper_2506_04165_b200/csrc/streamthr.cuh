@@ -421,10 +421,6 @@ __global__ void __launch_bounds__(kStNW * 32, 2) st_stream_kernel(StArgs a) {
       }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kStNW * 32) : "memory");
-#ifdef ATKG_ST_DEBUG
-    if (threadIdx.x == 0 && c < 3) printf("cta %u seg %u ctr %u bad %u Lc %08x\n", c, seg, fl_ctr, fl_bad, Lc);
-    if (c < 2 && lane == 0) printf("cta %u seg %u warp %d n %u tkey %08x bad %u r %u\n", c, seg, warp, w.n, w.tkey, w.bad, w.r);
-#endif
     if (threadIdx.x == 0) {
       sl[0] = (fl_bad || fl_ctr > kStSlotCap) ? kStBadCount : fl_ctr;
       sl[1] = Lc;
@@ -804,9 +800,6 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
   __syncthreads();
   const uint32_t ne_all = sh_ne;
   bool fast = sh_bad == 0 && Lk > kStKeyNegInf && !a.force_slow && ne_all <= a.ecap;
-#ifdef ATKG_ST_DEBUG
-  if (t == 0 && row < 3) printf("row %llu nslots %u ca %u cb %u seg_a %u bad %u Lk %08x E %u ne %u\n", (unsigned long long)row, nslots, ca, cb, seg_a, sh_bad, Lk, E, ne_all);
-#endif
   if (fast) {
     const uint32_t ne = ne_all;
     {
@@ -865,9 +858,6 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
   }
   __syncthreads();
   uint32_t M = sh_nc;
-#ifdef ATKG_ST_DEBUG
-  if (t == 0 && row < 3) printf("row %llu fast %d M %u m %u\n", (unsigned long long)row, (int)fast, M, sh_m);
-#endif
   if (!fast && a.gate) {  // giant row: the host reruns the exact path
     if (t == 0) atomicOr(a.gate, 1u);
     return;
