@@ -27,6 +27,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "emit.cuh"
 #include "ptx.cuh"
 #include "stage1.cuh"
 #include "stage2.cuh"
@@ -490,6 +491,30 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
   if (!out_v) return;  // stage-1 only (uniform across the CTA)
   __syncthreads();
   uint32_t nsort = P;
+  if constexpr (K32) {
+    // large candidate sets, one row per CTA: counting-sort rank emit over the
+    // value code, only the bins before rank k ranked (the dead row buffer
+    // holds the scratch); rows with -inf candidates (repeatable sentinel
+    // keys) or crowded bins take the radix-select path below
+    if (P > 512u && P <= 1024u && R == 1 && filled * B * 4 <= row_bytes) {  // measured: slower at 4096
+      __shared__ uint32_t rr_sent;
+      if (threadIdx.x == 0) rr_sent = 0;
+      __syncthreads();
+      const uint32_t M = filled * B;
+      uint32_t sflag = 0;
+      for (uint32_t q = threadIdx.x; q < M; q += blockDim.x)
+        sflag |= key32_value_bf16(rkeys[q]) == neg_inf() ? 1u : 0u;
+      if (sflag) atomicOr(&rr_sent, 1u);
+      __syncthreads();
+      if (!rr_sent && emit_ranked<uint32_t>(rkeys, reinterpret_cast<uint32_t*>(smem_raw), M, k,
+                                            [&](uint32_t r, uint32_t key) {
+                                              out_v[row * k + r] = key32_value_bf16(key);
+                                              out_i[row * k + r] = key & 0xffffu;
+                                            }))
+        return;
+      __syncthreads();
+    }
+  }
   if (P > 512u) {
     // large candidate sets: radix-select the k smallest (unique) keys into
     // the front, then sort only those

@@ -90,10 +90,11 @@ StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint
   sp.vtot = rows * n / ve;
   if (sp.vtot >= (1ull << 50)) return sp;
   if (sp.vtot / std::max<uint64_t>(1, (uint64_t)sm_count()) >= (1ull << 31)) return sp;  // 32-bit piece offsets
-  sp.slot_bytes = (uint32_t)env_u64("ATKG_ST_STEP", 32768);  // bytes per CTA step
-  if (sp.slot_bytes != 16384 && sp.slot_bytes != 32768) return sp;
+  // bytes per CTA step = kStNW warps x 32 lanes x UNR 16-byte vectors, UNR in {4, 8}
+  sp.slot_bytes = (uint32_t)env_u64("ATKG_ST_STEP", (uint64_t)kStNW * 4096);
+  if (sp.slot_bytes != (uint32_t)kStNW * 2048 && sp.slot_bytes != (uint32_t)kStNW * 4096) return sp;
   sp.ns = 0;
-  const uint64_t per_sm = env_u64("ATKG_ST_CTAS", 2);
+  const uint64_t per_sm = env_u64("ATKG_ST_CTAS", 16 / kStNW);
   uint64_t G = (uint64_t)sm_count() * per_sm;
   G = std::max<uint64_t>(1, std::min<uint64_t>(G, sp.vtot / 1024));
   sp.psz = (sp.vtot + G - 1) / G;
@@ -178,10 +179,10 @@ void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, u
   f.gate = a.gate;
   g_prof.bracket_begin(st);
   if (dtype == ATKG_BF16) {
-    if (sp.slot_bytes == 32768) launch_stream<__nv_bfloat16, 8>(sp, a, st);
+    if (sp.slot_bytes == (uint32_t)kStNW * 4096) launch_stream<__nv_bfloat16, 8>(sp, a, st);
     else launch_stream<__nv_bfloat16, 4>(sp, a, st);
   } else {
-    if (sp.slot_bytes == 32768) launch_stream<float, 8>(sp, a, st);
+    if (sp.slot_bytes == (uint32_t)kStNW * 4096) launch_stream<float, 8>(sp, a, st);
     else launch_stream<float, 4>(sp, a, st);
   }
   g_prof.bracket_end(st);

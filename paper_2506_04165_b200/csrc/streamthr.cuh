@@ -45,7 +45,10 @@
 
 namespace atkg {
 
-constexpr int kStNW = 8;           // consumer warps per CTA
+#ifndef ATKG_ST_NW
+#define ATKG_ST_NW 8
+#endif
+constexpr int kStNW = ATKG_ST_NW;           // consumer warps per CTA
 #ifndef ATKG_ST_LOG
 #define ATKG_ST_LOG 256
 #endif
@@ -302,7 +305,7 @@ __device__ __forceinline__ uint32_t st_warp_rth16(const uint32_t (&k)[N], uint32
 constexpr int kStSlots = ATKG_ST_SLOTS;
 
 template <typename T, int UNR>
-__global__ void __launch_bounds__(kStNW * 32, 2) st_stream_kernel(StArgs a) {
+__global__ void __launch_bounds__(kStNW * 32, 16 / kStNW) st_stream_kernel(StArgs a) {
   extern __shared__ __align__(128) uint8_t st_smem[];
   using V = StVec<T>;
   constexpr int VE = V::VE;
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(kStNW * 32, 2) st_stream_kernel(StArgs a) {
 #pragma unroll
         for (int i = 0; i < kStNW; ++i) k8[i] = samp[i * 32 + lane];
         const float mu = a.lfac * (float)(st.len * VE);
-        const uint32_t sr = (uint32_t)fminf(256.f, ceilf(mu + 4.5f * sqrtf(mu) + 3.f));
+        const uint32_t sr = (uint32_t)fminf((float)(kStNW * 32), ceilf(mu + 4.5f * sqrtf(mu) + 3.f));
         const uint32_t t = st_warp_rth16<kStNW>(k8, sr);
         __syncwarp();
         if (lane == 0) samp[0] = t;
