@@ -157,6 +157,7 @@ void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, u
   a.rfac = sp.rfac;
   a.lfac = sp.lfac;
   a.cfac = sp.cfac;
+  a.warp_sample = (uint32_t)env_u64("ATKG_ST_WARP_SAMPLE", 0);
   a.slots = static_cast<uint32_t*>(ws);
   uint32_t* gate = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + (sp.ws_bytes - 256));
   a.gate = sp.giant ? gate : nullptr;

@@ -97,6 +97,7 @@ struct StArgs {
   float rfac;          // per-warp rank target: R = 8 + rfac * (warp share of the segment)
   float lfac;          // sampled start: expected sample count above the row's safe level, per element
   float cfac;          // entries kept per row segment: Rc = 8 + cfac * (segment elements)
+  uint32_t warp_sample;  // sampled start per warp (no CTA barrier) instead of per CTA
   uint32_t* slots;     // [G][smax][kStSlotWords]
   uint32_t* gate;      // giant rows: set by the finish kernel when a row needs the exact path
   uint32_t* status;
@@ -449,11 +450,15 @@ __global__ void __launch_bounds__(kStNW * 32, 16 / kStNW) st_stream_kernel(StArg
     const uint32_t wl = wlen_of(st);
     uint4 x[UNR];
     float m[UNR];  // per-vector maxima (NaN-propagating)
+    if (wl == WV) {  // full slot: plain loads
 #pragma unroll
-    for (int i = 0; i < UNR; ++i) {
-      x[i] = (uint32_t)(i * 32 + lane) < wl ? sl[i * 32 + lane] : pad;
-      m[i] = V::vmax(x[i]);
+      for (int i = 0; i < UNR; ++i) x[i] = sl[i * 32 + lane];
+    } else {
+#pragma unroll
+      for (int i = 0; i < UNR; ++i) x[i] = (uint32_t)(i * 32 + lane) < wl ? sl[i * 32 + lane] : pad;
     }
+#pragma unroll
+    for (int i = 0; i < UNR; ++i) m[i] = V::vmax(x[i]);
     float mx = m[0];
 #pragma unroll
     for (int i = 1; i < UNR; ++i) mx = fmax_nan(mx, m[i]);
@@ -461,6 +466,15 @@ __global__ void __launch_bounds__(kStNW * 32, 16 / kStNW) st_stream_kernel(StArg
       // sampled start: the s-th largest lane maximum of the segment's first
       // step is below the row's safe level with high probability; any start
       // value is exact (the slot records the threshold actually used)
+      uint32_t t0;
+      if (a.warp_sample) {
+        // per-warp sample: the warp's own 32 lane maxima, no CTA barrier
+        const uint32_t k1[1] = {mx != mx ? 0u : st_okey(mx)};
+        const uint32_t wl = wlen_of(st);
+        const float mu = a.lfac * (float)(wl * VE);
+        const uint32_t sr = (uint32_t)fminf(32.f, ceilf(mu + 4.5f * sqrtf(mu) + 3.f));
+        t0 = st_warp_rth16<1>(k1, sr);
+      } else {
       samp[warp * 32 + lane] = mx != mx ? 0u : st_okey(mx);
       asm volatile("bar.sync 1, %0;" ::"n"(kStNW * 32) : "memory");
       if (warp == 0) {
@@ -474,7 +488,8 @@ __global__ void __launch_bounds__(kStNW * 32, 16 / kStNW) st_stream_kernel(StArg
         if (lane == 0) samp[0] = t;
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kStNW * 32) : "memory");
-      const uint32_t t0 = samp[0];
+      t0 = samp[0];
+      }
       if (t0 > w.tkey) {
         w.tkey = t0;
         w.L = st_oval(t0);
