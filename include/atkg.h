@@ -116,7 +116,11 @@ int atkg_select_candidates(const float* d_vals, const uint32_t* d_idx, uint64_t 
                            float* d_out_vals, uint32_t* d_out_idx, void* d_ws, size_t ws_bytes,
                            uint32_t* d_status, void* stream);
 
-/* approx_top_k_batch: stage 1 + stage 2 per row -> [rows][global_k]. */
+/* approx_top_k_batch: stage 1 + stage 2 per row -> [rows][global_k].
+ * Asynchronous on `stream`, except for rows longer than 2^24 elements: the
+ * threshold stream then reads a 4-byte device gate after its finish kernel
+ * (one stream synchronisation) and reruns the exact path if a row's
+ * threshold failed -- the results are bit-identical either way. */
 int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_params* p,
                       float* d_out_vals, uint32_t* d_out_idx, void* d_ws, size_t ws_bytes,
                       uint32_t* d_status, void* stream);
