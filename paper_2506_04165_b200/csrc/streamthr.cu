@@ -67,7 +67,10 @@ void launch_finish(const StPlan& sp, uint64_t rows, const StFinArgs& a, cudaStre
     CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem_fin));
     attr = sp.smem_fin;
   }
-  launch_pdl(kern, (unsigned)rows, 256, sp.smem_fin, st, a);
+  // a few rows (the giant row): one CTA per row is latency-bound, so give it
+  // 32 warps; many rows: 8 warps per row, several rows per SM
+  const unsigned threads = rows < 64 ? 1024u : 256u;
+  launch_pdl(kern, (unsigned)rows, threads, sp.smem_fin, st, a);
 }
 
 }  // namespace

@@ -650,16 +650,16 @@ struct StFinArgs {
   uint32_t* status;
 };
 
-// one CTA (256 threads) per row.  smem: ent keys[ecap] | ent pos[ecap] |
+// one CTA (256 threads; 1024 for a few long rows) per row.  smem: ent keys[ecap] | ent pos[ecap] |
 // grouped keys[ecap] | grouped pos[ecap] | cnt[B] | off[B] | cur[B]; the
 // candidate keys (u64, <= max(B*K', ecap)) alias the first two arrays.
 template <typename T, int KP>
-__global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
+__global__ void __launch_bounds__(1024) st_finish_kernel(StFinArgs a) {
   extern __shared__ __align__(128) uint8_t st_smem[];
   uint8_t* smem = st_smem;
   __shared__ uint32_t sh_l, sh_ne, sh_nk, sh_bad, sh_nc, sh_m;
   __shared__ uint32_t pfx[kStMaxRowPieces + 1];
-  __shared__ uint64_t red64[16];
+  __shared__ uint64_t red64[32];
   const uint32_t t = threadIdx.x, nt = blockDim.x;
   const uint64_t row = blockIdx.x;
   constexpr int VE = 16 / sizeof(T);
@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(256) st_finish_kernel(StFinArgs a) {
   // some slot), entry counts -> prefix pfx[]
   const int lane = t & 31;
   uint32_t Lk;
-  if (nslots <= kStFewSlots && a.ecap >= 1024) {
+  if (nslots <= kStFewSlots && a.ecap >= 1024 && nt == 256) {
     // few slots (rows over a handful of pieces): every thread reads the
     // headers (broadcast) and, speculatively, its share of every slot's
     // entries in the same round trip; filter against L = max threshold
