@@ -69,7 +69,7 @@ void launch_finish(const StPlan& sp, uint64_t rows, const StFinArgs& a, cudaStre
   }
   // a few rows (the giant row): one CTA per row is latency-bound, so give it
   // 32 warps; many rows: 8 warps per row, several rows per SM
-  const unsigned threads = rows < 64 ? 1024u : 256u;
+  const unsigned threads = rows < 64 ? 1024u : (unsigned)env_u64("ATKG_ST_FIN_THREADS", 256);
   launch_pdl(kern, (unsigned)rows, threads, sp.smem_fin, st, a);
 }
 

@@ -693,11 +693,12 @@ __global__ void __launch_bounds__(1024) st_finish_kernel(StFinArgs a) {
   // some slot), entry counts -> prefix pfx[]
   const int lane = t & 31;
   uint32_t Lk;
-  if (nslots <= kStFewSlots && a.ecap >= 1024 && nt == 256) {
+  if (nslots <= kStFewSlots && a.ecap >= 1024 && nt >= 256 && kStSlotCap % nt == 0) {
     // few slots (rows over a handful of pieces): every thread reads the
     // headers (broadcast) and, speculatively, its share of every slot's
     // entries in the same round trip; filter against L = max threshold
-    constexpr uint32_t PER = kStSlotCap / 256;
+    constexpr uint32_t PER = kStSlotCap / 256;  // entries per thread at 256 threads
+    const uint32_t per = kStSlotCap / nt;
     uint32_t kk[kStFewSlots][PER], pp[kStFewSlots][PER], mq[kStFewSlots];
     Lk = 0;
     bool bad = false;
@@ -710,21 +711,23 @@ __global__ void __launch_bounds__(1024) st_finish_kernel(StFinArgs a) {
         bad |= mq[q] > kStSlotCap;
 #pragma unroll
         for (uint32_t i = 0; i < PER; ++i) {
-          kk[q][i] = sl[2 + i * 256 + (t & 255)];
-          pp[q][i] = sl[2 + kStSlotCap + i * 256 + (t & 255)];
+          if (i < per) {
+            kk[q][i] = sl[2 + i * nt + t];
+            pp[q][i] = sl[2 + kStSlotCap + i * nt + t];
+          }
         }
       } else {
         mq[q] = 0;
       }
     }
     if (t == 0) { sh_l = Lk; if (bad) sh_bad = 1u; }
-    if (!bad && nt == 256) {
+    if (!bad) {
 #pragma unroll
       for (uint32_t q = 0; q < kStFewSlots; ++q) {
 #pragma unroll
         for (uint32_t i = 0; i < PER; ++i) {
-          const uint32_t e = i * 256 + t;
-          if (e < mq[q] && kk[q][i] >= Lk) {
+          const uint32_t e = i * nt + t;
+          if (i < per && e < mq[q] && kk[q][i] >= Lk) {
             const uint32_t d = atomicAdd(&sh_ne, 1u);
             if (d < a.ecap) {
               ek[d] = kk[q][i];
