@@ -211,6 +211,9 @@ struct WordNet<float> {
 // CTA = R row groups of TPR threads (TPR a multiple of 32).
 // smem: R rows of n elements | R x key_stride candidate keys | R x 264 words
 // of select scratch (P > 512 only)
+#ifndef ATKG_RR_RANK_MIN
+#define ATKG_RR_RANK_MIN 512  // rank emit for P in (ATKG_RR_RANK_MIN, 1024]
+#endif
 constexpr int kRowFastChunks = 4;       // closed-form pass 2 for buckets of <= 128
 
 // first k of the merge of two ascending runs a[0..na), b[0..nb) of unique keys
@@ -496,7 +499,7 @@ row_resident_kernel(const T* __restrict__ in, uint64_t rows, uint32_t n, uint32_
     // value code, only the bins before rank k ranked (the dead row buffer
     // holds the scratch); rows with -inf candidates (repeatable sentinel
     // keys) or crowded bins take the radix-select path below
-    if (P > 512u && P <= 1024u && R == 1 && filled * B * 4 <= row_bytes) {  // measured: slower at 4096
+    if (P > (uint32_t)ATKG_RR_RANK_MIN && P <= 1024u && R == 1 && filled * B * 4 <= row_bytes) {  // measured: slower at 4096
       __shared__ uint32_t rr_sent;
       if (threadIdx.x == 0) rr_sent = 0;
       __syncthreads();
