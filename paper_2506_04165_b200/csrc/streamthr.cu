@@ -210,8 +210,9 @@ bool run_select_ranked(const float* vals, const uint32_t* idx, uint64_t rows, ui
   if (env_u64("ATKG_NO_RANK_SELECT", 0) || count <= 128 || count > 1024) return false;
   uint32_t P = 2;
   while (P < count) P <<= 1;
-  stage2_rank_kernel<<<(unsigned)rows, 128, (size_t)P * 16, st>>>(vals, idx, (uint32_t)count, stride, k, limit, P,
-                                                                     ov, oi, status);
+  const unsigned threads = (unsigned)env_u64("ATKG_S2_THREADS", 128);
+  stage2_rank_kernel<<<(unsigned)rows, threads, (size_t)P * 16, st>>>(vals, idx, (uint32_t)count, stride, k, limit,
+                                                                       P, ov, oi, status);
   check_launch();
   return true;
 }

@@ -595,7 +595,7 @@ __device__ __forceinline__ bool st_emit_ranked(const uint64_t* keys, uint32_t* m
 // (index < limit) compacted into shared memory, then the counting-sort rank
 // emit; rows holding -inf (sentinel keys may repeat) or crowded bins sort
 // with a bitonic network instead.  smem: keys[P] | mem[P] (u64).
-__global__ void __launch_bounds__(128) stage2_rank_kernel(const float* __restrict__ vals,
+__global__ void __launch_bounds__(512) stage2_rank_kernel(const float* __restrict__ vals,
                                                           const uint32_t* __restrict__ idx, uint32_t count,
                                                           uint64_t stride, uint32_t k, uint64_t index_limit,
                                                           uint32_t P, float* out_v, uint32_t* out_i,
