@@ -57,6 +57,7 @@ extern "C" {
 #define ATKG_EINFEASIBLE 3    /* atk::NoFeasibleConfigError */
 #define ATKG_ECUDA 4          /* CUDA runtime failure */
 #define ATKG_EUNSUPPORTED 5   /* shape outside what the device path implements */
+#define ATKG_EFORMAT 6        /* atk::DatasetFormatError (dataset.hpp:14-16) */
 
 #define ATKG_FLAG_NAN 1u
 
@@ -225,6 +226,25 @@ typedef struct atkg_plan_result {
   int high_target_warning;
 } atkg_plan_result;
 int atkg_select_parameters(const atkg_plan_request* req, atkg_plan_result* out);
+
+/* ---- ATKV dataset container ------------------------------ */
+/* Replaces atk::read_dataset_file / write_dataset_file (dataset.hpp:45-49,
+ * dataset.cpp:45-124): "ATKV", version 1, rows u64 LE, dims u64 LE, then
+ * rows*dims fp32 LE.  Format failures return ATKG_EFORMAT with the reference's
+ * messages ("bad dataset magic", "dataset truncated: payload incomplete",
+ * "dataset payload contains NaN", ...).  Synchronous. */
+int atkg_dataset_read_header(const char* path, uint64_t* rows, uint64_t* dims);
+/* host buffer of `capacity` floats (ATKG_EINVAL if rows*dims exceeds it) */
+int atkg_dataset_read_file(const char* path, float* out, uint64_t capacity, uint64_t* rows,
+                           uint64_t* dims);
+int atkg_dataset_write_file(const char* path, const float* data, uint64_t rows, uint64_t dims);
+/* Device variants: the payload streams through pinned double-buffered chunks
+ * straight to/from HBM (16-byte aligned device buffer); NaN rejection is a
+ * device scan.  For dumping fused activations / replaying inputs. */
+int atkg_dataset_read_file_device(const char* path, float* d_out, uint64_t capacity,
+                                  uint64_t* rows, uint64_t* dims, void* stream);
+int atkg_dataset_write_file_device(const char* path, const float* d_in, uint64_t rows,
+                                   uint64_t dims, void* stream);
 
 /* ---- seeded synthetic inputs (documented convention) --------- */
 /* out[i] = mean + stddev * z_i, z from Box-Muller over xoshiro256++ streams

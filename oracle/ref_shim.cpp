@@ -17,6 +17,7 @@
 #include "atk/recall.hpp"
 #include "atk/topk.hpp"
 #include "atk/mips.hpp"
+#include "atk/dataset.hpp"
 
 namespace {
 thread_local std::string g_err;
@@ -26,6 +27,9 @@ int guard(F&& f) {
   try {
     f();
     return 0;
+  } catch (const atk::DatasetFormatError& e) {
+    g_err = e.what();
+    return 6;
   } catch (const atk::NoFeasibleConfigError& e) {
     g_err = e.what();
     return 3;
@@ -191,6 +195,27 @@ int ref_mips_fused(const float* database, uint64_t rows, uint64_t d, const float
       std::memcpy(ov + r * k, res.per_query[r].values.data(), 4ull * k);
       std::memcpy(oi + r * k, res.per_query[r].indices.data(), 4ull * k);
     }
+  });
+}
+
+// dataset.cpp:45-130 (ATKV container), file-path entry points
+int ref_dataset_write_file(const char* path, const float* data, uint64_t rows, uint64_t dims) {
+  return guard([&] {
+    atk::VectorDataset ds;
+    ds.rows = rows;
+    ds.dims = dims;
+    ds.data.assign(data, data + rows * dims);
+    atk::write_dataset_file(ds, path);
+  });
+}
+
+int ref_dataset_read_file(const char* path, float* out, uint64_t cap, uint64_t* rows, uint64_t* dims) {
+  return guard([&] {
+    const atk::VectorDataset ds = atk::read_dataset_file(path);
+    if (ds.data.size() > cap) throw std::invalid_argument("capacity");
+    std::memcpy(out, ds.data.data(), ds.data.size() * 4);
+    *rows = ds.rows;
+    *dims = ds.dims;
   });
 }
 

@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ATKG_LIB") or os.path.join(_HERE, "libatkg.so")  # override: experiments only
 
-ATKG_OK, ATKG_EINVAL, ATKG_ENAN, ATKG_EINFEASIBLE, ATKG_ECUDA, ATKG_EUNSUPPORTED = range(6)
+ATKG_OK, ATKG_EINVAL, ATKG_ENAN, ATKG_EINFEASIBLE, ATKG_ECUDA, ATKG_EUNSUPPORTED, ATKG_EFORMAT = range(7)
 ATKG_F32, ATKG_BF16 = 0, 1
 OP_STAGE1, OP_APPROX, OP_SELECT, OP_EXACT, OP_SUMMARY, OP_MERGE = range(6)
 FLAG_NAN = 1
@@ -20,6 +20,10 @@ FLAG_NAN = 1
 
 class NoFeasibleConfigError(RuntimeError):
     """atk::NoFeasibleConfigError (planner.hpp:14-16)."""
+
+
+class DatasetFormatError(RuntimeError):
+    """atk::DatasetFormatError (dataset.hpp:14-16)."""
 
 
 class Params(C.Structure):
@@ -81,6 +85,12 @@ def _load():
         "atkg_mc_expected_recall_adaptive": ([P, u64, f64p, f64p, C.POINTER(C.c_uint64)], i32),
         "atkg_legal_bucket_counts": ([u64, u64, vp, u64], u64),
         "atkg_select_parameters": ([C.POINTER(PlanRequestC), C.POINTER(PlanResultC)], i32),
+        "atkg_dataset_read_header": ([C.c_char_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], i32),
+        "atkg_dataset_read_file": ([C.c_char_p, vp, u64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], i32),
+        "atkg_dataset_write_file": ([C.c_char_p, vp, u64, u64], i32),
+        "atkg_dataset_read_file_device": ([C.c_char_p, vp, u64, C.POINTER(C.c_uint64),
+                                           C.POINTER(C.c_uint64), vp], i32),
+        "atkg_dataset_write_file_device": ([C.c_char_p, vp, u64, u64, vp], i32),
         "atkg_fill_normal": ([u64, u64, C.c_float, C.c_float, vp, u32], None),
         "atkg_fill_normal_range": ([u64, u64, u64, C.c_float, C.c_float, vp, u32], None),
         "atkg_f32_to_bf16": ([vp, u64, vp, u32], None),
@@ -109,6 +119,8 @@ def check(rc: int) -> None:
         raise ValueError(msg)
     if rc == ATKG_EINFEASIBLE:
         raise NoFeasibleConfigError(msg)
+    if rc == ATKG_EFORMAT:
+        raise DatasetFormatError(msg)
     if rc == ATKG_EUNSUPPORTED:
         raise NotImplementedError(msg)
     raise RuntimeError(msg)
