@@ -246,6 +246,20 @@ int atkg_dataset_read_file_device(const char* path, float* d_out, uint64_t capac
 int atkg_dataset_write_file_device(const char* path, const float* d_in, uint64_t rows,
                                    uint64_t dims, void* stream);
 
+/* ---- recall simulation ----------------------------------- */
+/* Rows [first_row, first_row + rows) of atk::synth_distinct (dataset.cpp:132-170):
+ * row r is a Fisher-Yates permutation of 1..n on derive_seed(seed, r); n <= 2^24.
+ * Host, `threads` workers. */
+int atkg_synth_distinct(uint64_t first_row, uint64_t rows, uint64_t n, uint64_t seed, float* out,
+                        uint32_t threads);
+/* atk::simulate_recall_many (simulate.hpp:31-34, simulate.cpp:53-113): rows
+ * generated on `threads` host workers, approx_top_k + recall counting on the
+ * device (stream), mean / sample stddev per config identical to the
+ * reference.  Synchronous. */
+int atkg_simulate_recall_many(const atkg_params* configs, uint32_t num_configs, uint64_t runs,
+                              uint64_t seed, uint32_t threads, double* mean_recall, double* stddev,
+                              void* stream);
+
 /* ---- seeded synthetic inputs (documented convention) --------- */
 /* out[i] = mean + stddev * z_i, z from Box-Muller over xoshiro256++ streams
  * derive_seed(seed, i / 65536) (rng.hpp:25-81), fp32. */

@@ -18,6 +18,7 @@
 #include "atk/topk.hpp"
 #include "atk/mips.hpp"
 #include "atk/dataset.hpp"
+#include "atk/simulate.hpp"
 
 namespace {
 thread_local std::string g_err;
@@ -216,6 +217,30 @@ int ref_dataset_read_file(const char* path, float* out, uint64_t cap, uint64_t* 
     std::memcpy(out, ds.data.data(), ds.data.size() * 4);
     *rows = ds.rows;
     *dims = ds.dims;
+  });
+}
+
+// dataset.cpp:132-150
+int ref_synth_distinct_row(uint64_t n, uint64_t seed, uint64_t row_index, float* out) {
+  return guard([&] {
+    const auto row = atk::synth_distinct_row(n, seed, row_index);
+    std::memcpy(out, row.data(), row.size() * 4);
+  });
+}
+
+// simulate.cpp:53-113; configs as (n, b, kp, k, lane) records
+int ref_simulate_recall_many(const uint64_t* cfg, uint32_t num, uint64_t runs, uint64_t seed,
+                             uint32_t threads, double* mean, double* sd) {
+  return guard([&] {
+    std::vector<atk::AlgoParams> ps;
+    for (uint32_t c = 0; c < num; ++c)
+      ps.push_back(mk(cfg[5 * c], cfg[5 * c + 1], static_cast<uint32_t>(cfg[5 * c + 2]),
+                      static_cast<uint32_t>(cfg[5 * c + 3]), static_cast<uint32_t>(cfg[5 * c + 4])));
+    const auto st = atk::simulate_recall_many(ps, runs, seed, threads);
+    for (uint32_t c = 0; c < num; ++c) {
+      mean[c] = st[c].mean_recall;
+      sd[c] = st[c].stddev;
+    }
   });
 }
 
