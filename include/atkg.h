@@ -252,8 +252,13 @@ int atkg_dataset_write_file_device(const char* path, const float* d_in, uint64_t
  * Host, `threads` workers. */
 int atkg_synth_distinct(uint64_t first_row, uint64_t rows, uint64_t n, uint64_t seed, float* out,
                         uint32_t threads);
+/* The same rows generated in HBM (one CTA per row, n <= 2^16, else
+ * ATKG_EUNSUPPORTED); bit-identical to atkg_synth_distinct. */
+int atkg_synth_distinct_device(uint64_t first_row, uint64_t rows, uint64_t n, uint64_t seed,
+                               float* d_out, void* stream);
 /* atk::simulate_recall_many (simulate.hpp:31-34, simulate.cpp:53-113): rows
- * generated on `threads` host workers, approx_top_k + recall counting on the
+ * generated on the device for n <= 2^16 (else on `threads` host workers),
+ * approx_top_k + recall counting on the
  * device (stream), mean / sample stddev per config identical to the
  * reference.  Synchronous. */
 int atkg_simulate_recall_many(const atkg_params* configs, uint32_t num_configs, uint64_t runs,

@@ -92,6 +92,7 @@ def _load():
                                            C.POINTER(C.c_uint64), vp], i32),
         "atkg_dataset_write_file_device": ([C.c_char_p, vp, u64, u64, vp], i32),
         "atkg_synth_distinct": ([u64, u64, u64, u64, vp, u32], i32),
+        "atkg_synth_distinct_device": ([u64, u64, u64, u64, vp, vp], i32),
         "atkg_simulate_recall_many": ([P, u32, u64, u64, u32, f64p, f64p, vp], i32),
         "atkg_fill_normal": ([u64, u64, C.c_float, C.c_float, vp, u32], None),
         "atkg_fill_normal_range": ([u64, u64, u64, C.c_float, C.c_float, vp, u32], None),

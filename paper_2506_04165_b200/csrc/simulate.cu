@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <thread>
 #include <vector>
@@ -109,6 +110,80 @@ __global__ void __launch_bounds__(256) recall_hits_kernel(const float* __restric
   if (lane == 0) hits[r] = c;
 }
 
+// Device Fisher-Yates, one CTA per row with the row in shared memory as u16
+// (value - 1; n <= 2^16 keeps 128 KB per row).  The swap chain is serial by
+// definition, so one thread walks it; the CTA fills and writes the row out
+// coalesced.  Draws are the host Xoshiro's, bit for bit (rng.hpp:34-81).
+constexpr uint64_t kDeviceSynthMaxN = 1ull << 16;
+
+__device__ __forceinline__ uint64_t d_splitmix(uint64_t& st) {
+  uint64_t z = (st += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t d_rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+__global__ void __launch_bounds__(128) synth_distinct_kernel(uint64_t first_row, uint64_t n, uint64_t seed,
+                                                             float* __restrict__ out) {
+  extern __shared__ uint16_t perm[];
+  const uint64_t row = first_row + blockIdx.x;
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) perm[i] = static_cast<uint16_t>(i);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // derive_seed(seed, row) (rng.hpp:25-32), then the xoshiro256++ state
+    uint64_t st = seed;
+    (void)d_splitmix(st);
+    st ^= 0x9e3779b97f4a7c15ull * (row + 1);
+    const uint64_t a = d_splitmix(st), b = d_splitmix(st);
+    uint64_t sm = a ^ (b >> 1), s0, s1, s2, s3;
+    s0 = d_splitmix(sm);
+    s1 = d_splitmix(sm);
+    s2 = d_splitmix(sm);
+    s3 = d_splitmix(sm);
+    for (uint64_t i = n - 1; i >= 1; --i) {
+      const uint64_t bound = i + 1;
+      uint64_t x = d_rotl(s0 + s3, 23) + s0;
+      uint64_t t = s1 << 17;
+      s2 ^= s0; s3 ^= s1; s1 ^= s2; s0 ^= s3; s2 ^= t; s3 = d_rotl(s3, 45);
+      uint64_t lo = x * bound, hi = __umul64hi(x, bound);
+      if (lo < bound) {
+        const uint64_t threshold = (0 - bound) % bound;
+        while (lo < threshold) {
+          x = d_rotl(s0 + s3, 23) + s0;
+          t = s1 << 17;
+          s2 ^= s0; s3 ^= s1; s1 ^= s2; s0 ^= s3; s2 ^= t; s3 = d_rotl(s3, 45);
+          lo = x * bound;
+          hi = __umul64hi(x, bound);
+        }
+      }
+      const uint16_t vi = perm[i], vj = perm[hi];
+      perm[i] = vj;
+      perm[hi] = vi;
+    }
+  }
+  __syncthreads();
+  float* o = out + blockIdx.x * n;
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) o[i] = static_cast<float>(perm[i]) + 1.0f;
+}
+
+void launch_synth_distinct(uint64_t first_row, uint64_t rows, uint64_t n, uint64_t seed, float* d_out,
+                           cudaStream_t s) {
+  if (rows == 0) return;
+  const size_t smem = n * sizeof(uint16_t);
+  static bool attr = false;
+  if (!attr) {
+    CUDA_OK(cudaFuncSetAttribute(synth_distinct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kDeviceSynthMaxN * sizeof(uint16_t))));
+    attr = true;
+  }
+  for (uint64_t r0 = 0; r0 < rows; r0 += 65535) {
+    const unsigned g = static_cast<unsigned>(std::min<uint64_t>(65535, rows - r0));
+    synth_distinct_kernel<<<g, 128, smem, s>>>(first_row + r0, n, seed, d_out + r0 * n);
+    check_launch();
+  }
+}
+
 struct Pinned {
   void* p = nullptr;
   ~Pinned() {
@@ -138,6 +213,16 @@ int atkg_synth_distinct(uint64_t first_row, uint64_t rows, uint64_t n, uint64_t 
   });
 }
 
+int atkg_synth_distinct_device(uint64_t first_row, uint64_t rows, uint64_t n, uint64_t seed, float* d_out,
+                               void* stream) {
+  return guarded([&] {
+    check_synth_n(n);
+    if (n > kDeviceSynthMaxN) throw Unsupported("synth_distinct on the device: n must be <= 2^16");
+    if (rows && !d_out) throw Inval("output buffer must not be null");
+    launch_synth_distinct(first_row, rows, n, seed, d_out, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int atkg_simulate_recall_many(const atkg_params* configs, uint32_t num_configs, uint64_t runs,
                               uint64_t seed, uint32_t threads, double* mean_recall, double* stddev,
                               void* stream) {
@@ -156,8 +241,12 @@ int atkg_simulate_recall_many(const atkg_params* configs, uint32_t num_configs, 
 
     // Batches of runs: about 32 MiB of rows (at least one row per worker) per
     // pinned buffer, so pinning stays cheap and generation overlaps the GPU.
+    // Rows of n <= 2^16 are generated on the device (synth_distinct_kernel):
+    // no host generation, no H2D; larger rows come from host workers.
+    const bool dev_gen = n <= kDeviceSynthMaxN && !std::getenv("ATKG_SIM_HOST_GEN");
     const uint64_t workers = std::max<uint32_t>(threads, 1);
-    const uint64_t batch = std::min<uint64_t>(runs, std::max<uint64_t>(workers, (1ull << 23) / n));
+    const uint64_t batch = dev_gen ? std::min<uint64_t>(runs, 2048)
+                                   : std::min<uint64_t>(runs, std::max<uint64_t>(workers, (1ull << 23) / n));
     uint32_t kmax = 0;
     size_t ws = 0;
     for (uint32_t c = 0; c < num_configs; ++c) {
@@ -169,7 +258,8 @@ int atkg_simulate_recall_many(const atkg_params* configs, uint32_t num_configs, 
     }
     Pinned host[2], hits_h;
     Device d_rows, d_vals, d_idx, d_ws, d_hits, d_status;
-    for (auto& h : host) CUDA_OK(cudaHostAlloc(&h.p, batch * n * 4, cudaHostAllocDefault));
+    if (!dev_gen)
+      for (auto& h : host) CUDA_OK(cudaHostAlloc(&h.p, batch * n * 4, cudaHostAllocDefault));
     CUDA_OK(cudaHostAlloc(&hits_h.p, size_t(num_configs) * runs * 4, cudaHostAllocDefault));
     CUDA_OK(cudaMalloc(&d_rows.p, batch * n * 4));
     CUDA_OK(cudaMalloc(&d_vals.p, batch * kmax * 4));
@@ -193,12 +283,16 @@ int atkg_simulate_recall_many(const atkg_params* configs, uint32_t num_configs, 
       const uint64_t r0 = bi * batch, nr = std::min(batch, runs - r0);
       synth_rows(r0, nr, n, seed, static_cast<float*>(host[bi & 1].p), threads);
     };
-    gen(0);
+    if (!dev_gen) gen(0);
     uint32_t* hits = static_cast<uint32_t*>(d_hits.p);
     for (uint64_t bi = 0; bi < nbatches; ++bi) {
       const uint64_t r0 = bi * batch, nr = std::min(batch, runs - r0);
-      CUDA_OK(cudaMemcpyAsync(d_rows.p, host[bi & 1].p, nr * n * 4, cudaMemcpyHostToDevice, s));
-      CUDA_OK(cudaEventRecord(copied[bi & 1], s));
+      if (dev_gen) {
+        launch_synth_distinct(r0, nr, n, seed, static_cast<float*>(d_rows.p), s);
+      } else {
+        CUDA_OK(cudaMemcpyAsync(d_rows.p, host[bi & 1].p, nr * n * 4, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaEventRecord(copied[bi & 1], s));
+      }
       for (uint32_t c = 0; c < num_configs; ++c) {
         const int rc = atkg_approx_top_k(ATKG_F32, d_rows.p, nr, &configs[c], static_cast<float*>(d_vals.p),
                                          static_cast<uint32_t*>(d_idx.p), d_ws.p, ws,
@@ -212,7 +306,7 @@ int atkg_simulate_recall_many(const atkg_params* configs, uint32_t num_configs, 
       }
       // generate the next batch while the GPU works on this one; the buffer it
       // overwrites was last read by the copy of batch bi - 1
-      if (bi + 1 < nbatches) {
+      if (!dev_gen && bi + 1 < nbatches) {
         CUDA_OK(cudaEventSynchronize(copied[(bi + 1) & 1]));
         gen(bi + 1);
       }

@@ -35,6 +35,17 @@ def synth_distinct(rows: int, n: int, seed: int, first_row: int = 0, threads: in
     return out
 
 
+def synth_distinct_device(rows: int, n: int, seed: int, first_row: int = 0, device=None) -> "torch.Tensor":
+    """Same rows generated in HBM (n <= 2^16): [rows, n] fp32 CUDA tensor."""
+    import torch
+    from .topk import _stream_ptr
+    dev = torch.device(device if device is not None else "cuda")
+    out = torch.empty((rows, n), dtype=torch.float32, device=dev)
+    _lib.check(_lib.lib.atkg_synth_distinct_device(first_row, rows, n, seed, out.data_ptr() if out.numel() else None,
+                                                   _stream_ptr(out.device)))
+    return out
+
+
 def synth_distinct_row(n: int, seed: int, row_index: int) -> np.ndarray:
     return synth_distinct(1, n, seed, first_row=row_index, threads=1)[0]
 

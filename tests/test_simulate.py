@@ -97,3 +97,35 @@ def test_simulate_single_and_batched_runs(cuda, ref):
     st = atk.simulate_recall(big, 130, 77, threads=16, device=cuda)
     mean, sd = ref_simulate(ref.lib, [big], 130, 77, threads=16)
     assert (st.mean_recall, st.stddev) == (mean[0], sd[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,seed,first", [(1, 3, 0), (2, 0, 5), (1000, 7, 1), (4096, 2**63 + 5, 9), (65536, 12345, 100)])
+def test_synth_distinct_device_bit_exact(cuda, n, seed, first):
+    import paper_2506_04165_b200 as atk
+    rows = 37
+    d = atk.synth_distinct_device(rows, n, seed, first_row=first, device=cuda).cpu().numpy()
+    h = atk.synth_distinct(rows, n, seed, first_row=first, threads=8)
+    assert np.array_equal(d, h)
+
+
+@pytest.mark.gpu
+def test_synth_distinct_device_limits(cuda):
+    import paper_2506_04165_b200 as atk
+    with pytest.raises(NotImplementedError, match="n must be <= 2\\^16"):
+        atk.synth_distinct_device(1, 65537, 0, device=cuda)
+    with pytest.raises(ValueError, match="^synth_distinct: n must be >= 1$"):
+        atk.synth_distinct_device(1, 0, 0, device=cuda)
+
+
+@pytest.mark.gpu
+def test_simulate_device_and_host_generation_agree(cuda, ref, monkeypatch):
+    import paper_2506_04165_b200 as atk
+    configs = [atk.AlgoParams(n=65536, num_buckets=256, local_k=2, global_k=64),
+               atk.AlgoParams(n=65536, num_buckets=512, local_k=1, global_k=128)]
+    dev = atk.simulate_recall_many(configs, 300, 31, device=cuda)
+    monkeypatch.setenv("ATKG_SIM_HOST_GEN", "1")
+    host = atk.simulate_recall_many(configs, 300, 31, device=cuda)
+    mean, sd = ref_simulate(ref.lib, configs, 300, 31)
+    for c in range(2):
+        assert (dev[c].mean_recall, dev[c].stddev) == (host[c].mean_recall, host[c].stddev) == (mean[c], sd[c])
