@@ -181,6 +181,12 @@ int atkg_fused_workspace_size(uint64_t m, uint64_t kdim, const atkg_params* p, s
 int atkg_gemm_bf16(const void* d_x, const void* d_w_t, uint64_t m, uint64_t kdim, uint64_t n,
                    float* d_out, void* stream);
 
+/* fp32 MIPS scores, bit-identical to atk::score_block (mips.hpp:57-63,
+ * mips.cpp:57-91): out[q*out_stride + c] = <queries[q], database[c]> for
+ * c < n, -inf for n <= c < n_padded (mips.cpp:112). Device pointers. */
+int atkg_mips_score(const float* d_queries, uint64_t b, const float* d_database, uint64_t n,
+                    uint64_t d, float* d_out, uint64_t out_stride, uint64_t n_padded, void* stream);
+
 /* ---- host-buffer drop-in entry points (synchronous) --------------------- */
 int atkg_stage1_host(const float* in, uint64_t rows, const atkg_params* p, float* grid_vals,
                      uint32_t* grid_idx);

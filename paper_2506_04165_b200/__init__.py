@@ -6,6 +6,8 @@ in include/atkg.h); this package is the host-side mirror of the reference
 interface.  Importing fails loudly if the library has not been built.
 """
 from ._lib import NoFeasibleConfigError  # noqa: F401
+from .mips import (MipsResult, MipsStats, default_block_cols, mips_fused, mips_unfused,  # noqa: F401
+                   validate_mips_request)
 from .simulate import (SimStats, simulate_recall, simulate_recall_many, synth_distinct,  # noqa: F401
                        synth_distinct_device, synth_distinct_row)
 from .dataset import (DatasetFormatError, VectorDataset, read_dataset_file, read_dataset_to_device,  # noqa: F401

@@ -91,6 +91,7 @@ def _load():
         "atkg_dataset_read_file_device": ([C.c_char_p, vp, u64, C.POINTER(C.c_uint64),
                                            C.POINTER(C.c_uint64), vp], i32),
         "atkg_dataset_write_file_device": ([C.c_char_p, vp, u64, u64, vp], i32),
+        "atkg_mips_score": ([vp, u64, vp, u64, u64, vp, u64, u64, vp], i32),
         "atkg_synth_distinct": ([u64, u64, u64, u64, vp, u32], i32),
         "atkg_synth_distinct_device": ([u64, u64, u64, u64, vp, vp], i32),
         "atkg_simulate_recall_many": ([P, u32, u64, u64, u32, f64p, f64p, vp], i32),

@@ -1,0 +1,93 @@
+// mips.cu -- fp32 MIPS scoring for the mips_unfused / mips_fused mirror.
+//
+// score_block (mips.cpp:57-91): out[q, c] = sum_j queries[q, j] * database[c, j],
+// one fp32 accumulator from 0, j ascending, multiply and add rounded
+// separately (the reference builds with -ffp-contract=off).  Columns
+// [n, n_padded) get -inf (mips.cpp:112).  The kernel keeps that exact order
+// per output, so the scores -- and every top-k built on them -- are
+// bit-identical to the reference.  64x64 output tiles staged through shared
+// memory in 32-wide slices of the dimension; 4x4 outputs per thread.
+//
+// The bf16 tcgen05 path with stage 1 in the epilogue is atkg_fused_gemm_top_k
+// (fused_gemm.cu); this one is the fp32 reference-exact scorer.
+#include <cuda_runtime.h>
+
+#include "internal.hpp"
+
+namespace atkg {
+namespace {
+
+constexpr int kTile = 64, kSlice = 32;
+
+__global__ void __launch_bounds__(256) mips_score_kernel(const float* __restrict__ q, uint64_t b,
+                                                         const float* __restrict__ db, uint64_t n,
+                                                         uint64_t d, float* __restrict__ out,
+                                                         uint64_t stride, uint64_t n_padded) {
+  __shared__ float qs[kSlice][kTile + 1];
+  __shared__ float ws[kSlice][kTile + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const uint64_t q0 = uint64_t(blockIdx.y) * kTile, c0 = uint64_t(blockIdx.x) * kTile;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+  for (uint64_t j0 = 0; j0 < d; j0 += kSlice) {
+    for (int e = threadIdx.x; e < kTile * kSlice; e += 256) {
+      const int r = e / kSlice, j = e % kSlice;
+      const uint64_t qq = q0 + r, cc = c0 + r, jj = j0 + j;
+      qs[j][r] = (qq < b && jj < d) ? q[qq * d + jj] : 0.0f;
+      ws[j][r] = (cc < n && jj < d) ? db[cc * d + jj] : 0.0f;
+    }
+    __syncthreads();
+    const int jn = static_cast<int>(d - j0 < uint64_t(kSlice) ? d - j0 : kSlice);
+    for (int j = 0; j < jn; ++j) {
+      float a[4], w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = qs[j][ty * 4 + i];
+        w[i] = ws[j][tx * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[i][k] = __fadd_rn(acc[i][k], __fmul_rn(a[i], w[k]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint64_t qq = q0 + ty * 4 + i;
+    if (qq >= b) continue;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t cc = c0 + tx * 4 + k;
+      if (cc < n)
+        out[qq * stride + cc] = acc[i][k];
+      else if (cc < n_padded)
+        out[qq * stride + cc] = -__int_as_float(0x7f800000);
+    }
+  }
+}
+
+}  // namespace
+}  // namespace atkg
+
+using namespace atkg;
+
+extern "C" int atkg_mips_score(const float* d_queries, uint64_t b, const float* d_database, uint64_t n,
+                               uint64_t d, float* d_out, uint64_t out_stride, uint64_t n_padded,
+                               void* stream) {
+  return guarded([&] {
+    if (d == 0) throw Inval("mips: dims must be >= 1");
+    if (n == 0) throw Inval("mips: database must not be empty");
+    if (b == 0) throw Inval("mips: queries must not be empty");
+    if (n_padded < n || out_stride < n_padded) throw Inval("mips: out_stride >= n_padded >= n required");
+    if (!d_queries || !d_database || !d_out) throw Inval("mips: null buffer");
+    const uint64_t gx = (n_padded + kTile - 1) / kTile, gy = (b + kTile - 1) / kTile;
+    if (gx > 0x7fffffffull || gy > 65535) throw Unsupported("mips: shape exceeds the launch grid");
+    mips_score_kernel<<<dim3(unsigned(gx), unsigned(gy)), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        d_queries, b, d_database, n, d, d_out, out_stride, n_padded);
+    check_launch();
+  });
+}
