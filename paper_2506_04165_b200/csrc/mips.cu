@@ -5,8 +5,8 @@
 // separately (the reference builds with -ffp-contract=off).  Columns
 // [n, n_padded) get -inf (mips.cpp:112).  The kernel keeps that exact order
 // per output, so the scores -- and every top-k built on them -- are
-// bit-identical to the reference.  64x64 output tiles staged through shared
-// memory in 32-wide slices of the dimension; 4x4 outputs per thread.
+// bit-identical to the reference.  128x128 output tiles staged through shared
+// memory in 16-wide slices of the dimension; 8x8 outputs per thread.
 //
 // The bf16 tcgen05 path with stage 1 in the epilogue is atkg_fused_gemm_top_k
 // (fused_gemm.cu); this one is the fp32 reference-exact scorer.
@@ -17,51 +17,53 @@
 namespace atkg {
 namespace {
 
-constexpr int kTile = 64, kSlice = 32;
+constexpr int kTile = 128, kSlice = 16, kPer = 8;  // 128x128 tile, 8x8 outputs per thread
 
 __global__ void __launch_bounds__(256) mips_score_kernel(const float* __restrict__ q, uint64_t b,
                                                          const float* __restrict__ db, uint64_t n,
                                                          uint64_t d, float* __restrict__ out,
                                                          uint64_t stride, uint64_t n_padded) {
-  __shared__ float qs[kSlice][kTile + 1];
-  __shared__ float ws[kSlice][kTile + 1];
+  __shared__ __align__(16) float qs[kSlice][kTile];
+  __shared__ __align__(16) float ws[kSlice][kTile];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const uint64_t q0 = uint64_t(blockIdx.y) * kTile, c0 = uint64_t(blockIdx.x) * kTile;
-  float acc[4][4];
+  float acc[kPer][kPer];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < kPer; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (int j = 0; j < kPer; ++j) acc[i][j] = 0.0f;
   for (uint64_t j0 = 0; j0 < d; j0 += kSlice) {
+#pragma unroll
     for (int e = threadIdx.x; e < kTile * kSlice; e += 256) {
       const int r = e / kSlice, j = e % kSlice;
       const uint64_t qq = q0 + r, cc = c0 + r, jj = j0 + j;
-      qs[j][r] = (qq < b && jj < d) ? q[qq * d + jj] : 0.0f;
-      ws[j][r] = (cc < n && jj < d) ? db[cc * d + jj] : 0.0f;
+      qs[j][r] = (qq < b && jj < d) ? __ldg(q + qq * d + jj) : 0.0f;
+      ws[j][r] = (cc < n && jj < d) ? __ldg(db + cc * d + jj) : 0.0f;
     }
     __syncthreads();
     const int jn = static_cast<int>(d - j0 < uint64_t(kSlice) ? d - j0 : kSlice);
     for (int j = 0; j < jn; ++j) {
-      float a[4], w[4];
+      float a[kPer], w[kPer];
+      const float4 a0 = *reinterpret_cast<const float4*>(&qs[j][ty * kPer]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&qs[j][ty * kPer + 4]);
+      const float4 w0 = *reinterpret_cast<const float4*>(&ws[j][tx * kPer]);
+      const float4 w1 = *reinterpret_cast<const float4*>(&ws[j][tx * kPer + 4]);
+      a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w; a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+      w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w; w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        a[i] = qs[j][ty * 4 + i];
-        w[i] = ws[j][tx * 4 + i];
-      }
+      for (int i = 0; i < kPer; ++i)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) acc[i][k] = __fadd_rn(acc[i][k], __fmul_rn(a[i], w[k]));
+        for (int k = 0; k < kPer; ++k) acc[i][k] = __fadd_rn(acc[i][k], __fmul_rn(a[i], w[k]));
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint64_t qq = q0 + ty * 4 + i;
+  for (int i = 0; i < kPer; ++i) {
+    const uint64_t qq = q0 + ty * kPer + i;
     if (qq >= b) continue;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint64_t cc = c0 + tx * 4 + k;
+    for (int k = 0; k < kPer; ++k) {
+      const uint64_t cc = c0 + tx * kPer + k;
       if (cc < n)
         out[qq * stride + cc] = acc[i][k];
       else if (cc < n_padded)
