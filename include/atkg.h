@@ -245,7 +245,7 @@ int atkg_dataset_read_file(const char* path, float* out, uint64_t capacity, uint
                            uint64_t* dims);
 int atkg_dataset_write_file(const char* path, const float* data, uint64_t rows, uint64_t dims);
 /* Device variants: the payload streams through pinned double-buffered chunks
- * straight to/from HBM (16-byte aligned device buffer); NaN rejection is a
+ * straight to/from HBM; NaN rejection is a
  * device scan.  For dumping fused activations / replaying inputs. */
 int atkg_dataset_read_file_device(const char* path, float* d_out, uint64_t capacity,
                                   uint64_t* rows, uint64_t* dims, void* stream);

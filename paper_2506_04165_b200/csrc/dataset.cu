@@ -99,12 +99,14 @@ bool host_has_nan(const float* x, uint64_t count) {
   return any != 0;
 }
 
-// HBM-bound NaN scan: 16-byte loads, grid-stride, one atomic per warp that sees a NaN.
+// HBM-bound NaN scan: 16-byte loads when the buffer is 16-byte aligned (scalar
+// loads otherwise, e.g. a row-offset view), grid-stride, one atomic per warp that
+// sees a NaN.
 __global__ void __launch_bounds__(256) nan_scan_kernel(const float* __restrict__ x, uint64_t count,
-                                                       uint32_t* __restrict__ flag) {
+                                                       bool vec, uint32_t* __restrict__ flag) {
   const uint64_t tid = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   const uint64_t nthreads = uint64_t(gridDim.x) * blockDim.x;
-  const uint64_t nvec = count / 4;
+  const uint64_t nvec = vec ? count / 4 : 0;
   const uint4* v = reinterpret_cast<const uint4*>(x);
   bool nan = false;
   for (uint64_t i = tid; i < nvec; i += nthreads) {
@@ -113,17 +115,17 @@ __global__ void __launch_bounds__(256) nan_scan_kernel(const float* __restrict__
            ((w.z & 0x7fffffffu) > 0x7f800000u) | ((w.w & 0x7fffffffu) > 0x7f800000u);
   }
   for (uint64_t i = nvec * 4 + tid; i < count; i += nthreads)
-    nan |= (__float_as_uint(x[i]) & 0x7fffffffu) > 0x7f800000u;
+    nan |= (__float_as_uint(__ldg(x + i)) & 0x7fffffffu) > 0x7f800000u;
   if (__any_sync(0xffffffffu, nan) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
 void launch_nan_scan(const float* d, uint64_t count, uint32_t* flag, cudaStream_t s) {
   if (count == 0) return;
-  if (reinterpret_cast<uintptr_t>(d) % 16 != 0) throw Inval("device buffer must be 16-byte aligned");
-  const uint64_t want = (count / 4 + 255) / 256;
+  const bool vec = reinterpret_cast<uintptr_t>(d) % 16 == 0;
+  const uint64_t want = ((vec ? count / 4 : count) + 255) / 256;
   const uint64_t cap = uint64_t(sm_count()) * 8;
   const unsigned grid = static_cast<unsigned>(want < 1 ? 1 : (want > cap ? cap : want));
-  nan_scan_kernel<<<grid, 256, 0, s>>>(d, count, flag);
+  nan_scan_kernel<<<grid, 256, 0, s>>>(d, count, vec, flag);
   check_launch();
 }
 

@@ -171,12 +171,9 @@ void launch_synth_distinct(uint64_t first_row, uint64_t rows, uint64_t n, uint64
                            cudaStream_t s) {
   if (rows == 0) return;
   const size_t smem = n * sizeof(uint16_t);
-  static bool attr = false;
-  if (!attr) {
-    CUDA_OK(cudaFuncSetAttribute(synth_distinct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(kDeviceSynthMaxN * sizeof(uint16_t))));
-    attr = true;
-  }
+  // the opt-in shared-memory limit is per device: set it on every call (cheap)
+  CUDA_OK(cudaFuncSetAttribute(synth_distinct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(kDeviceSynthMaxN * sizeof(uint16_t))));
   for (uint64_t r0 = 0; r0 < rows; r0 += 65535) {
     const unsigned g = static_cast<unsigned>(std::min<uint64_t>(65535, rows - r0));
     synth_distinct_kernel<<<g, 128, smem, s>>>(first_row + r0, n, seed, d_out + r0 * n);

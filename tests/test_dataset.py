@@ -242,3 +242,22 @@ def test_device_read_feeds_approx_top_k(cuda, tmp_path):
     ev, ei = O.port().approx_top_k_batch(x.reshape(rows, dims), 256, 2, 64)
     assert np.array_equal(v.cpu().numpy(), ev)
     assert np.array_equal(i.cpu().numpy().astype(np.uint32), ei)
+
+
+@pytest.mark.gpu
+def test_device_write_from_unaligned_view(cuda, tmp_path):
+    """A row-offset view (not 16-byte aligned) takes the scalar NaN scan."""
+    import torch
+    import paper_2506_04165_b200 as atk
+    rows, dims = 7, 1001
+    x = golden_payload(rows, dims)
+    base = torch.zeros(1 + rows * dims, dtype=torch.float32, device=cuda)
+    base[1:] = torch.from_numpy(x).to(cuda)
+    view = base[1:].view(rows, dims)
+    assert view.data_ptr() % 16 != 0
+    p = tmp_path / "u.atkv"
+    atk.write_dataset_from_device(view, p)
+    assert p.read_bytes() == _header(rows, dims) + x.astype("<f4").tobytes()
+    base[-1] = float("nan")
+    with pytest.raises(atk.DatasetFormatError, match="^dataset payload contains NaN$"):
+        atk.write_dataset_from_device(view, p)
