@@ -25,8 +25,8 @@ __global__ void __launch_bounds__(256, 2) mips_score_kernel(const float* __restr
                                                             uint64_t stride, uint64_t n_padded) {
   // two slice buffers: the global loads of slice s+1 are in flight (registers)
   // while slice s is multiplied out of shared memory
-  __shared__ __align__(16) float qs[2][kSlice][kTile];
-  __shared__ __align__(16) float ws[2][kSlice][kTile];
+  __shared__ __align__(16) float qs[2][kSlice][kTile + 4];  // +4: the transposing stores hit 16 banks, not 2
+  __shared__ __align__(16) float ws[2][kSlice][kTile + 4];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const uint64_t q0 = uint64_t(blockIdx.y) * kTile, c0 = uint64_t(blockIdx.x) * kTile;
   constexpr int kLoads = kTile * kSlice / 256;
