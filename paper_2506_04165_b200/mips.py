@@ -20,7 +20,8 @@ import numpy as np
 
 from . import _lib
 from .dataset import VectorDataset
-from .topk import AlgoParams, TopKResult, _stream_ptr, select_candidates_device, stage1_device
+from .topk import (AlgoParams, TopKResult, _check_device_status, _status, _stream_ptr, select_candidates_device,
+                   stage1_device)
 
 try:
     import torch
@@ -101,13 +102,15 @@ def mips_top_k_device(queries: "torch.Tensor", database: "torch.Tensor", params:
     filled = min(padded.local_k, padded.n // padded.num_buckets) * padded.num_buckets
     chunk = max(1, min(b, _SCORE_BUDGET // (padded.n * 4)))
     vs, is_ = [], []
+    st = _status(queries.device)  # one status word, checked once after every chunk is queued
     for q0 in range(0, b, chunk):
         scores = score_block_device(queries[q0:q0 + chunk], database, padded.n)
-        gv, gi = stage1_device(scores, padded)
-        v, i = select_candidates_device(gv, gi, params.global_k, index_limit=n, count=filled)
+        gv, gi = stage1_device(scores, padded, status=st)
+        v, i = select_candidates_device(gv, gi, params.global_k, index_limit=n, count=filled, status=st)
         vs.append(v)
         is_.append(i)
         del scores, gv, gi
+    _check_device_status(st, queries.device)
     return torch.cat(vs), torch.cat(is_)
 
 

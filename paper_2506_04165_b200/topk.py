@@ -309,8 +309,9 @@ def approx_top_k_device(x: "torch.Tensor", params: AlgoParams, status=None, out=
 
 
 def select_candidates_device(vals: "torch.Tensor", idx: "torch.Tensor", k: int,
-                             index_limit: int = 2**64 - 1, count: int | None = None):
-    """Per-row stage 2 over [rows, C] candidate tensors."""
+                             index_limit: int = 2**64 - 1, count: int | None = None, status=None):
+    """Per-row stage 2 over [rows, C] candidate tensors.  Pass a zeroed int32
+    `status` tensor to skip the per-call synchronising check."""
     rows, stride = vals.shape
     count = stride if count is None else count
     dev = vals.device
@@ -318,11 +319,12 @@ def select_candidates_device(vals: "torch.Tensor", idx: "torch.Tensor", k: int,
     ws = workspace(_ws_size(_lib.OP_SELECT, 0, rows, p), dev)
     ov = torch.empty((rows, k), dtype=torch.float32, device=dev)
     oi = torch.empty((rows, k), dtype=torch.int32, device=dev)
-    st = _status(dev)
+    st = status if status is not None else _status(dev)
     check(lib.atkg_select_candidates(vals.contiguous().data_ptr(), idx.contiguous().data_ptr(), rows, count, stride,
                                      k, min(index_limit, 2**64 - 1), ov.data_ptr(), oi.data_ptr(), ws.data_ptr(),
                                      ws.numel(), st.data_ptr(), _stream_ptr(dev)))
-    _check_device_status(st, dev)
+    if status is None:
+        _check_device_status(st, dev)
     return ov, oi
 
 
