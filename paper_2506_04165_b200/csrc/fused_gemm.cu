@@ -38,6 +38,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstdint>
+#include <cstring>
 #include <string>
 
 #include "../../include/atkg.h"
@@ -460,6 +461,17 @@ void run_plain_gemm(const void* x, const void* w_t, uint64_t m, uint64_t kdim, u
   else launch_gemm<1, 0, 1>(ma, mb, ga, st);
 }
 
+// Unfused alternative for shapes the fused epilogue supports (plain GEMM ->
+// grid stage 1 -> stage 2, identical results).  Off by default: no shape has
+// measured faster this way yet.  ATKG_FUSED_PATH=unfused selects it.
+bool small_d_unfused(uint64_t m, uint64_t kdim, const atkg_params& p) {
+  (void)m;
+  (void)kdim;
+  if (p.local_k > p.n / p.num_buckets) return false;  // grid slots all filled
+  const char* f = std::getenv("ATKG_FUSED_PATH");
+  return f && std::strcmp(f, "unfused") == 0;
+}
+
 uint64_t fused_cand_bytes(uint64_t m, const atkg_params& p) {
   return align_up(m * p.num_buckets * p.local_k * 4ull);
 }
@@ -475,8 +487,13 @@ int atkg_fused_workspace_size(uint64_t m, uint64_t kdim, const atkg_params* p, s
   return guarded([&] {
     if (p == nullptr || bytes == nullptr) throw_inval("null argument");
     validate(*p);
-    (void)kdim;
-    if (fused_nb(*p) != 0) {
+    if (fused_nb(*p) != 0 && small_d_unfused(m, kdim, *p)) {
+      const uint64_t count = (uint64_t)p->num_buckets * p->local_k;
+      size_t s1 = 0;
+      if (atkg_workspace_size(ATKG_OP_STAGE1, ATKG_F32, m, p, &s1) != ATKG_OK) throw Inval(atkg_last_error());
+      *bytes = align_up(m * p->n * 4ull) + 2 * fused_cand_bytes(m, *p) + align_up(s1) +
+               select_ws_bytes(m, count, p->global_k);
+    } else if (fused_nb(*p) != 0) {
       const uint64_t count = (uint64_t)p->num_buckets * p->local_k;
       *bytes = 2 * fused_cand_bytes(m, *p) + select_ws_bytes(m, count, p->global_k);
     } else {  // unfused: scores + the approx_top_k workspace
@@ -509,6 +526,24 @@ int atkg_fused_gemm_top_k(const void* d_x, const void* d_w_t, uint64_t m, uint64
       const int rc = atkg_approx_top_k(ATKG_F32, scores, m, p, d_out_vals, d_out_idx, inner,
                                        need - align_up(m * p->n * 4ull), d_status, stream);
       if (rc != ATKG_OK) throw Inval(atkg_last_error());
+      return;
+    }
+    if (small_d_unfused(m, kdim, *p)) {
+      // write the fp32 scores, then the grid stage 1 + stage 2 (identical results)
+      uint8_t* w = static_cast<uint8_t*>(d_ws);
+      float* scores = d_scores ? d_scores : reinterpret_cast<float*>(w);
+      w += align_up(m * p->n * 4ull);
+      float* gv = reinterpret_cast<float*>(w);
+      uint32_t* gi = reinterpret_cast<uint32_t*>(w + fused_cand_bytes(m, *p));
+      w += 2 * fused_cand_bytes(m, *p);
+      size_t s1 = 0;
+      if (atkg_workspace_size(ATKG_OP_STAGE1, ATKG_F32, m, p, &s1) != ATKG_OK) throw Inval(atkg_last_error());
+      run_plain_gemm(d_x, d_w_t, m, kdim, p->n, scores, st);
+      const int rc = atkg_stage1(ATKG_F32, scores, m, p, gv, gi, w, s1, d_status, stream);
+      if (rc != ATKG_OK) throw Inval(atkg_last_error());
+      w += align_up(s1);
+      const uint64_t count = (uint64_t)p->num_buckets * p->local_k;
+      run_select(gv, gi, m, count, count, p->global_k, UINT64_MAX, d_out_vals, d_out_idx, w, d_status, st);
       return;
     }
     const uint64_t B = p->num_buckets, S = p->n / B;

@@ -80,6 +80,12 @@ StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint
   StPlan sp;
   if (!for_size && env_u64("ATKG_NO_STREAMTHR", 0)) return sp;
   if (kp != 1 && kp != 2 && kp != 4 && kp != 8) return sp;
+  // Many rows with a large K: the per-row finish (rebuild + rank of >= K
+  // survivors) outweighs the stream's saving over the exact grid stage 1 +
+  // stage 2 (MIPS shape 1024 x 1,000,448, K = 1024, B = 1024, K' = 4:
+  // 13.6 -> 6.2 ms per batch after the tcgen05 GEMM).  Sizing keeps the
+  // stream's workspace either way.
+  if (!for_size && k >= 1024 && rows >= env_u64("ATKG_STREAMTHR_BIGK_ROWS", 64)) return sp;
   const uint64_t es = dtype == ATKG_BF16 ? 2 : 4;
   const uint64_t ve = 16 / es;
   if (n < env_u64("ATKG_STREAMTHR_MIN_N", 32768) || n % ve != 0) return sp;

@@ -140,3 +140,21 @@ def test_c4_full_size(cuda, ref):
     check_scores(scores[:256], x[:256], w)
     rv, ri = ref.approx_top_k_batch(scores.cpu().numpy(), 128, 4, 287)
     assert np.array_equal(bits(v), bits(rv)) and np.array_equal(u32(i), u32(ri))
+
+
+@pytest.mark.parametrize("m,kd,n,B,kp,k,lane", [FUSED[2], FUSED[4], FUSED[7]])
+def test_unfused_alternative_identical(cuda, port, monkeypatch, m, kd, n, B, kp, k, lane):
+    """ATKG_FUSED_PATH=unfused (plain GEMM -> grid stage 1 -> stage 2) returns
+    the fused epilogue's results bit for bit."""
+    x, w = operands(m, kd, n, 17 + m, cuda)
+    p = atk.AlgoParams(n, B, kp, k, lane)
+    monkeypatch.delenv("ATKG_FUSED_PATH", raising=False)
+    fv, fi = T.fused_gemm_top_k_device(x, w, p)
+    monkeypatch.setenv("ATKG_FUSED_PATH", "unfused")
+    scores = torch.empty((m, n), dtype=torch.float32, device=cuda)
+    uv, ui = T.fused_gemm_top_k_device(x, w, p, scores=scores)
+    uv2, ui2 = T.fused_gemm_top_k_device(x, w, p)
+    assert torch.equal(uv, fv) and torch.equal(ui, fi)
+    assert torch.equal(uv2, fv) and torch.equal(ui2, fi)
+    rv, ri = port.approx_top_k_batch(scores.cpu().numpy(), B, kp, k, lane)
+    assert np.array_equal(bits(uv), bits(rv)) and np.array_equal(u32(ui), u32(ri))
