@@ -88,6 +88,15 @@ const char* atkg_version(void);
  * (cudaSetDevice of the library's runtime). */
 int atkg_set_device(int device);
 
+/* Process-wide path-selection overrides, for tests and tuning only (no
+ * effect on results: every path is bit-identical).  Unset options keep the
+ * measured production choice; value UINT64_MAX resets one.  Names:
+ *   no_streamthr, streamthr_force_slow, streamthr_giant_n, no_rowthr,
+ *   rowthr, no_rowres, short_force_slow, no_short, fused_path (0 auto,
+ *   1 unfused), sim_host_gen, no_pdl. */
+int atkg_set_option(const char* name, uint64_t value);
+uint64_t atkg_get_option(const char* name, uint64_t dflt);
+
 int atkg_validate(const atkg_params* p);
 int atkg_validate_analysis(const atkg_params* p);
 

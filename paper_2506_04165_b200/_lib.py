@@ -57,6 +57,8 @@ def _load():
         "atkg_last_error": ([], C.c_char_p),
         "atkg_version": ([], C.c_char_p),
         "atkg_set_device": ([i32], i32),
+        "atkg_set_option": ([C.c_char_p, u64], i32),
+        "atkg_get_option": ([C.c_char_p, u64], u64),
         "atkg_validate": ([P], i32),
         "atkg_validate_analysis": ([P], i32),
         "atkg_workspace_size": ([i32, i32, u64, P, sz], i32),
@@ -128,6 +130,26 @@ def check(rc: int) -> None:
     if rc == ATKG_EUNSUPPORTED:
         raise NotImplementedError(msg)
     raise RuntimeError(msg)
+
+
+def set_option(name: str, value: int | None) -> None:
+    """Path-selection override (atkg_set_option); None restores the default."""
+    check(lib.atkg_set_option(name.encode(), 2**64 - 1 if value is None else int(value)))
+
+
+class option:
+    """Context manager: `with option("st_force_slow", 1): ...` (tests)."""
+
+    def __init__(self, name: str, value: int):
+        self.name, self.value = name, value
+
+    def __enter__(self):
+        self.prev = lib.atkg_get_option(self.name.encode(), 2**64 - 1)
+        set_option(self.name, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        set_option(self.name, None if self.prev == 2**64 - 1 else self.prev)
 
 
 def make_params(n: int, num_buckets: int, local_k: int, global_k: int, lane_multiple: int = 128) -> Params:

@@ -32,13 +32,77 @@ constexpr int kSegWarps = 8;   // warps (= segments) per stage-1 CTA
 constexpr int kPrefetch = 4;   // stride-rows per batch in the stage-1 loop
 constexpr uint32_t kMaxSortKeys = 16384;  // one CTA's shared-memory sort (128 KB)
 
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return dev;
+}
+
 int sm_count() {
-  static int n = [] {
-    int dev = 0, c = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
-    return c > 0 ? c : 148;
-  }();
+  static std::atomic<int> cache[kMaxDevices] = {};
+  const int dev = current_device();
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    int c = 0;
+    if (cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || c <= 0) c = 148;
+    cache[dev].store(c, std::memory_order_relaxed);
+    n = c;
+  }
   return n;
+}
+
+void ensure_smem(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, const void*>, size_t>> done;  // (device, kernel) -> bytes set
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : done)
+    if (e.first.first == dev && e.first.second == kern) {
+      if (e.second >= bytes) return;
+      CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      e.second = bytes;
+      return;
+    }
+  CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  done.push_back({{dev, kern}, bytes});
+}
+
+namespace {
+struct OptSlot {
+  char name[48];
+  std::atomic<uint64_t> val;
+};
+constexpr int kMaxOpts = 64;
+OptSlot g_opts[kMaxOpts];
+std::atomic<int> g_nopts{0};
+std::mutex g_opt_mu;
+}  // namespace
+
+uint64_t opt(const char* name, uint64_t dflt) {
+  const int n = g_nopts.load(std::memory_order_acquire);
+  for (int i = 0; i < n; ++i)
+    if (std::strcmp(g_opts[i].name, name) == 0) {
+      const uint64_t v = g_opts[i].val.load(std::memory_order_relaxed);
+      return v == ~0ull ? dflt : v;
+    }
+  return dflt;
+}
+
+void set_opt(const char* name, uint64_t v) {
+  if (!name || std::strlen(name) >= sizeof(OptSlot::name)) throw_inval("option name too long");
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  const int n = g_nopts.load(std::memory_order_relaxed);
+  for (int i = 0; i < n; ++i)
+    if (std::strcmp(g_opts[i].name, name) == 0) {
+      g_opts[i].val.store(v, std::memory_order_relaxed);
+      return;
+    }
+  if (n >= kMaxOpts) throw_inval("too many options");
+  std::strcpy(g_opts[n].name, name);
+  g_opts[n].val.store(v, std::memory_order_relaxed);
+  g_nopts.store(n + 1, std::memory_order_release);
 }
 
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
@@ -114,11 +178,6 @@ constexpr size_t flat_smem() {
   return flat_smem_bytes<T, KP, flat_vec(KP, sizeof(T)), kFlatWarps, kFlatSlots, kFlatRows, kLogCap>();
 }
 
-uint64_t env_u64(const char* name, uint64_t dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::strtoull(e, nullptr, 10) : dflt;
-}
-
 template <typename T>
 int flat_occupancy(uint32_t kp) {
   const void* k = nullptr;
@@ -129,23 +188,25 @@ int flat_occupancy(uint32_t kp) {
 #undef ATKG_OCC
     default: return 1;
   }
-  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_smem(k, smem);
   int n = 0;
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kFlatWarps * 32, smem));
   return n > 0 ? n : 1;
 }
 
 int flat_ctas_per_sm(int dtype, uint32_t kp) {
-  static int cache[2][17] = {};
-  int& c = cache[dtype == ATKG_BF16 ? 1 : 0][kp <= 16 ? kp : 0];
-  if (c == 0) {
-    int dev = 0, cc = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return 2;
+  static std::atomic<int> cache[kMaxDevices][2][17] = {};
+  const int dev = current_device();
+  std::atomic<int>& c = cache[dev][dtype == ATKG_BF16 ? 1 : 0][kp <= 16 ? kp : 0];
+  int v = c.load(std::memory_order_relaxed);
+  if (v == 0) {
+    int cc = 0;
     cudaDeviceGetAttribute(&cc, cudaDevAttrComputeCapabilityMajor, dev);
     if (cc < 10) return 2;  // planning without an sm_100 device (workspace sizing)
-    c = dtype == ATKG_BF16 ? flat_occupancy<__nv_bfloat16>(kp) : flat_occupancy<float>(kp);
+    v = dtype == ATKG_BF16 ? flat_occupancy<__nv_bfloat16>(kp) : flat_occupancy<float>(kp);
+    c.store(v, std::memory_order_relaxed);
   }
-  return c;
+  return v;
 }
 
 struct S1Plan {
@@ -172,13 +233,13 @@ S1Plan plan_stage1(int dtype, const void* in, uint64_t rows, uint64_t len, uint6
   if (!kp_specialised(kp) || pl.nstr == 0) return pl;
   const int Vf = flat_vec(kp, esz);
   const bool tma_ok = (addr % 16 == 0) && ((row_stride * esz) % 16 == 0) && ((B * esz) % 16 == 0) && (B % Vf == 0);
-  if (tma_ok && env_u64("ATKG_NO_FLAT", 0) == 0) {
+  if (tma_ok && opt("no_flat", 0) == 0) {
     pl.kind = S1Plan::kFlat;
     pl.V = Vf;
     pl.tiles = static_cast<uint32_t>(ceil_div(B, 32ull * Vf));
     pl.units = rows * pl.tiles;
     pl.total = pl.units * pl.nstr;
-    const uint64_t target = env_u64("ATKG_WARPS", static_cast<uint64_t>(sm_count()) * flat_ctas_per_sm(dtype, kp) * kFlatWarps);
+    const uint64_t target = opt("flat_warps", static_cast<uint64_t>(sm_count()) * flat_ctas_per_sm(dtype, kp) * kFlatWarps);
     pl.len = std::max<uint64_t>(1, ceil_div(pl.total, std::max<uint64_t>(1, target)));
     pl.warps = ceil_div(pl.total, pl.len);
     pl.parts = static_cast<uint32_t>(ceil_div(pl.nstr, pl.len) + 1);
@@ -230,11 +291,7 @@ void launch_stage1(const S1Plan& pl, const void* in, uint64_t rows, uint64_t row
     a.status = status;
     auto kern = flat_kernel_fn<T, KP>();
     constexpr size_t smem = flat_smem<T, KP>();
-    static bool attr = false;
-    if (!attr) {
-      CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
+    ensure_smem_fn(kern, smem);
     g_prof.bracket_begin(st);
     kern<<<static_cast<unsigned>(ceil_div(pl.warps, kFlatWarps)), kFlatWarps * 32, smem, st>>>(a);
     check_launch();
@@ -257,11 +314,7 @@ void launch_stage1(const S1Plan& pl, const void* in, uint64_t rows, uint64_t row
   a.out = out;
   a.status = status;
   auto kern = stage1_segments_kernel<T, KP, 4, kSegWarps, kPrefetch>;
-  static bool attr = false;
-  if (!attr) {
-    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    attr = true;
-  }
+  ensure_smem_fn(kern, 160 * 1024);
   g_prof.bracket_begin(st);
   kern<<<static_cast<unsigned>(ceil_div(pl.groups, kSegWarps / pl.group)), kSegWarps * 32, pl.smem, st>>>(a);
   check_launch();
@@ -348,7 +401,7 @@ RowPlan plan_rowres(int dtype, const void* in, uint64_t n, uint64_t B, uint32_t 
   RowPlan rp;
   const uint64_t esz = dtype == ATKG_BF16 ? 2 : 4, E = 4 / esz;
   const uint64_t row_bytes = n * esz;
-  if (!kp_specialised(kp) || env_u64("ATKG_NO_ROWRES", 0)) return rp;
+  if (!kp_specialised(kp) || opt("no_rowres", 0)) return rp;
   if (row_bytes > 64 * 1024 || row_bytes % 16 != 0 || reinterpret_cast<uintptr_t>(in) % 16 != 0) return rp;
   if (B % E != 0 || n / B > 4096) return rp;
   const uint64_t filled = std::min<uint64_t>(kp, n / B) * B;
@@ -362,7 +415,7 @@ RowPlan plan_rowres(int dtype, const void* in, uint64_t n, uint64_t B, uint32_t 
   const size_t scratch = 264 * 4;
   const size_t per_row = ((row_bytes + 127) & ~127ull) + keys + scratch;
   // small CTAs (one row when rows are large) keep many rows in flight per SM
-  const uint64_t rmax = env_u64("ATKG_ROWRES_R", 0);
+  const uint64_t rmax = opt("rowres_rows", 0);
   rp.R = static_cast<uint32_t>(
       rmax ? rmax : std::max<uint64_t>(1, std::min<uint64_t>(128 / rp.TPR, (48 * 1024) / per_row)));
   // pass 2 reads whole 32/E-row windows: rows past the end land in the
@@ -371,7 +424,7 @@ RowPlan plan_rowres(int dtype, const void* in, uint64_t n, uint64_t B, uint32_t 
   const size_t over = (size_t)((CH - nstr % CH) % CH) * B * esz;  // window overrun past the row
   const size_t tail = rp.R * (keys + scratch);
   const size_t pad = over > tail ? over - tail : 0;
-  rp.fast = (nstr <= 128 && pad <= 4096 && !env_u64("ATKG_RR_SLOW", 0)) ? 1u : 0u;
+  rp.fast = (nstr <= 128 && pad <= 4096 && !opt("rowres_slow", 0)) ? 1u : 0u;
   rp.smem = rp.R * per_row + (rp.fast ? pad : 0);
   rp.ok = true;
   return rp;
@@ -380,11 +433,7 @@ template <typename T, int KP>
 void launch_rowres(const RowPlan& rp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t k,
                    float* ov, uint32_t* oi, float* gv, uint32_t* gi, uint32_t* status, cudaStream_t st) {
   auto kern = row_resident_kernel<T, KP>;
-  static size_t attr = 0;
-  if (attr < rp.smem) {
-    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rp.smem));
-    attr = rp.smem;
-  }
+  ensure_smem_fn(kern, rp.smem);
   const uint32_t filled = (uint32_t)std::min<uint64_t>(KP, n / B);
   g_prof.bracket_begin(st);
   kern<<<static_cast<unsigned>(ceil_div(rows, rp.R)), rp.R * rp.TPR, rp.smem, st>>>(
@@ -461,11 +510,7 @@ void run_radix(const Src& src, uint64_t rows, uint64_t count, uint32_t k, float*
   radix_gather_kernel<Src><<<grid, 256, 0, st>>>(src, sel, keys, k);
   check_launch();
   const uint32_t P = next_pow2(k);
-  static bool attr = false;
-  if (!attr) {
-    CUDA_OK(cudaFuncSetAttribute(sort_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSortKeys * 8));
-    attr = true;
-  }
+  ensure_smem_fn(sort_emit_kernel, kMaxSortKeys * 8);
   sort_emit_kernel<<<static_cast<unsigned>(rows), std::min<uint32_t>(1024, P / 2), P * 8, st>>>(keys, k, P, ov, oi,
                                                                                              status);
   check_launch();
@@ -495,12 +540,7 @@ void run_select(const float* vals, const uint32_t* idx, uint64_t rows, uint64_t 
     return;
   }
   if (P <= kMaxSortKeys) {
-    static bool attr = false;
-    if (!attr) {
-      CUDA_OK(cudaFuncSetAttribute(stage2_bitonic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kMaxSortKeys * 8));
-      attr = true;
-    }
+    ensure_smem_fn(stage2_bitonic_kernel, kMaxSortKeys * 8);
     stage2_bitonic_kernel<<<static_cast<unsigned>(rows), std::min<uint32_t>(1024, P / 2), P * 8, st>>>(
         vals, idx, count, stride, k, limit, P, ov, oi, status);
     check_launch();
@@ -530,11 +570,7 @@ template <int KP>
 void launch_merge_select(const S1Plan& pl, const atkg_params& p, const uint32_t* ws, uint64_t rows, float* ov,
                          uint32_t* oi, float* gv, uint32_t* gi, uint32_t* status, cudaStream_t st) {
   const size_t smem = merge_select_smem(pl, p);
-  static size_t attr = 0;
-  if (attr < smem) {
-    CUDA_OK(cudaFuncSetAttribute(merge_select_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  ensure_smem_fn(merge_select_kernel<KP>, smem);
   const uint32_t P = next_pow2(filled_count(p));
   const uint32_t threads = std::min<uint32_t>(512, std::max<uint32_t>(64, (uint32_t)std::max<uint64_t>(p.num_buckets, P / 2)));
   const uint32_t filled = (uint32_t)std::min<uint64_t>(p.local_k, p.n / p.num_buckets);
@@ -569,9 +605,19 @@ struct HostCtx {
     return stream;
   }
 };
+// one context per device: its stream and buffers live on that device
 HostCtx& host_ctx() {
-  static HostCtx* c = new HostCtx();
-  return *c;
+  static HostCtx* ctx[kMaxDevices] = {};
+  static std::mutex mu;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ctx[dev]) ctx[dev] = new HostCtx();
+  return *ctx[dev];
+}
+
+// caller-supplied workspace must cover what the dispatch will use
+void check_ws(size_t have, size_t need) {
+  if (have < need) throw_inval("workspace smaller than atkg_workspace_size");
 }
 
 void check_status_sync(const uint32_t* d_status, cudaStream_t st) {
@@ -580,6 +626,75 @@ void check_status_sync(const uint32_t* d_status, cudaStream_t st) {
   CUDA_OK(cudaStreamSynchronize(st));
   if (flags & ATKG_FLAG_NAN) throw NanInput();
   if (flags & kFlagFew) throw_inval("fewer candidates than k");
+}
+
+// workspace bytes for `op` (atkg_workspace_size): the maximum over every
+// dispatch path the call may take, for 16-byte aligned and unaligned inputs
+size_t ws_need_uncached(int op, int dtype, uint64_t rows, const atkg_params& pr) {
+  const atkg_params* p = &pr;
+  size_t bytes = 0;
+  for (uintptr_t addr : {uintptr_t(256), uintptr_t(264), uintptr_t(258)}) {
+    const void* in = reinterpret_cast<const void*>(addr);
+    size_t b = 0;
+    switch (op) {
+      case ATKG_OP_STAGE1: {
+        const S1Plan pl = plan_stage1(dtype, in, rows, p->n, p->n, p->num_buckets, p->local_k);
+        b = stage1_ws_bytes(pl, rows, p->num_buckets, p->local_k);
+        break;
+      }
+      case ATKG_OP_APPROX: {
+        const S1Plan pl = plan_stage1(dtype, in, rows, p->n, p->n, p->num_buckets, p->local_k);
+        b = stage1_ws_bytes(pl, rows, p->num_buckets, p->local_k) + grid_bytes(rows, *p) +
+            select_ws_bytes(rows, filled_count(*p), p->global_k);
+        const ThrPlan tp = plan_rowthr(dtype, in, p->n, p->num_buckets, p->local_k, p->global_k);
+        if (tp.ok) b = std::max<size_t>(b, rowthr_ws_bytes(rows, tp));
+        const StPlan sp = plan_streamthr(dtype, in, rows, p->n, p->num_buckets, p->local_k, p->global_k, true);
+        if (sp.ok) b = std::max<size_t>(b, sp.ws_bytes);
+        break;
+      }
+      case ATKG_OP_SELECT:
+        b = select_ws_bytes(rows, p->n, p->global_k);
+        break;
+      case ATKG_OP_EXACT:
+        b = radix_ws_bytes(rows, p->global_k);
+        break;
+      case ATKG_OP_SUMMARY: {
+        const S1Plan pl = plan_stage1(dtype, in, 1, p->n, p->n, p->num_buckets, p->local_k);
+        b = stage1_ws_bytes(pl, 1, p->num_buckets, p->local_k);
+        break;
+      }
+      case ATKG_OP_MERGE:
+        b = grid_bytes(1, *p) + select_ws_bytes(1, filled_count(*p), p->global_k);
+        break;
+      default:
+        throw_inval("unknown workspace op");
+    }
+    bytes = std::max(bytes, b);
+  }
+  // slack so every device path can align its pointers
+  return bytes + 512;
+}
+
+// memoised per thread: the check runs on every call (host critical path)
+size_t ws_need(int op, int dtype, uint64_t rows, const atkg_params& p) {
+  struct Ent {
+    int op, dtype, dev;
+    uint64_t rows;
+    atkg_params p;
+    size_t bytes;
+  };
+  thread_local Ent memo[8];
+  thread_local int next = 0;
+  const int dev = current_device();
+  for (const Ent& e : memo)
+    if (e.bytes && e.op == op && e.dtype == dtype && e.dev == dev && e.rows == rows && e.p.n == p.n &&
+        e.p.num_buckets == p.num_buckets && e.p.local_k == p.local_k && e.p.global_k == p.global_k &&
+        e.p.lane_multiple == p.lane_multiple)
+      return e.bytes;
+  const size_t b = ws_need_uncached(op, dtype, rows, p);
+  memo[next] = Ent{op, dtype, dev, rows, p, b};
+  next = (next + 1) % 8;
+  return b;
 }
 
 }  // namespace atkg
@@ -595,6 +710,12 @@ const char* atkg_version(void) { return "atkg 0.1 (sm_100a)"; }
 int atkg_set_device(int device) {
   return guarded([&] { CUDA_OK(cudaSetDevice(device)); });
 }
+
+int atkg_set_option(const char* name, uint64_t value) {
+  return guarded([&] { set_opt(name, value); });
+}
+
+uint64_t atkg_get_option(const char* name, uint64_t dflt) { return opt(name, dflt); }
 
 void atkg_profile_begin(void) { atkg_profile_begin_every(1); }
 
@@ -628,44 +749,7 @@ int atkg_validate(const atkg_params* p) {
 }
 
 int atkg_workspace_size(int op, int dtype, uint64_t rows, const atkg_params* p, size_t* bytes) {
-  return guarded([&] {
-    const void* aligned = reinterpret_cast<const void*>(static_cast<uintptr_t>(256));
-    switch (op) {
-      case ATKG_OP_STAGE1: {
-        const S1Plan pl = plan_stage1(dtype, aligned, rows, p->n, p->n, p->num_buckets, p->local_k);
-        *bytes = stage1_ws_bytes(pl, rows, p->num_buckets, p->local_k);
-        break;
-      }
-      case ATKG_OP_APPROX: {
-        const S1Plan pl = plan_stage1(dtype, aligned, rows, p->n, p->n, p->num_buckets, p->local_k);
-        *bytes = stage1_ws_bytes(pl, rows, p->num_buckets, p->local_k) + grid_bytes(rows, *p) +
-                 select_ws_bytes(rows, filled_count(*p), p->global_k);
-        const ThrPlan tp = plan_rowthr(dtype, aligned, p->n, p->num_buckets, p->local_k, p->global_k);
-        if (tp.ok) *bytes = std::max<size_t>(*bytes, rowthr_ws_bytes(rows, tp));
-        const StPlan sp = plan_streamthr(dtype, aligned, rows, p->n, p->num_buckets, p->local_k, p->global_k, true);
-        if (sp.ok) *bytes = std::max<size_t>(*bytes, sp.ws_bytes);
-        break;
-      }
-      case ATKG_OP_SELECT:
-        *bytes = select_ws_bytes(rows, p->n, p->global_k);
-        break;
-      case ATKG_OP_EXACT:
-        *bytes = radix_ws_bytes(rows, p->global_k);
-        break;
-      case ATKG_OP_SUMMARY: {
-        const S1Plan pl = plan_stage1(dtype, aligned, 1, p->n, p->n, p->num_buckets, p->local_k);
-        *bytes = stage1_ws_bytes(pl, 1, p->num_buckets, p->local_k);
-        break;
-      }
-      case ATKG_OP_MERGE:
-        *bytes = grid_bytes(1, *p) + select_ws_bytes(1, filled_count(*p), p->global_k);
-        break;
-      default:
-        throw_inval("unknown workspace op");
-    }
-    // slack so every device path can align its pointers
-    *bytes += 512;
-  });
+  return guarded([&] { *bytes = ws_need(op, dtype, rows, *p); });
 }
 
 int atkg_stage1(int dtype, const void* d_in, uint64_t rows, const atkg_params* p, float* d_grid_vals,
@@ -673,7 +757,7 @@ int atkg_stage1(int dtype, const void* d_in, uint64_t rows, const atkg_params* p
   return guarded([&] {
     validate(*p);
     if (rows == 0) return;
-    (void)ws_bytes;
+    check_ws(ws_bytes, ws_need(ATKG_OP_STAGE1, dtype, rows, *p));
     run_stage1_grid(dtype, d_in, rows, *p, d_grid_vals, d_grid_idx, (uint64_t)p->local_k * p->num_buckets, d_ws,
                     d_status, static_cast<cudaStream_t>(stream));
   });
@@ -686,7 +770,7 @@ int atkg_select_candidates(const float* d_vals, const uint32_t* d_idx, uint64_t 
     if (k == 0) throw_inval("k must be >= 1");
     if (rows == 0) return;
     if (count < k) throw_inval("fewer candidates than k");
-    (void)ws_bytes;
+    check_ws(ws_bytes, ws_need(ATKG_OP_SELECT, ATKG_F32, rows, atkg_params{count, 1, 1, k, 1}));
     run_select(d_vals, d_idx, rows, count, stride, k, index_limit, d_out_vals, d_out_idx, d_ws, d_status,
                static_cast<cudaStream_t>(stream));
   });
@@ -697,7 +781,7 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
   return guarded([&] {
     validate(*p);
     if (rows == 0) return;
-    (void)ws_bytes;
+    check_ws(ws_bytes, ws_need(ATKG_OP_APPROX, dtype, rows, *p));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const StPlan sp = plan_streamthr(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
     if (sp.ok) {  // long rows: threshold stream + per-row finish (exact fallback per row)
@@ -721,11 +805,6 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     float* gv = reinterpret_cast<float*>(w);
     uint32_t* gi = reinterpret_cast<uint32_t*>(w + rows * gstride * 4);
     w += grid_bytes(rows, *p);
-    const PipePlan pp = plan_rowpipe(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
-    if (pp.ok) {  // bf16 rows in shared memory: persistent row pipeline, row threshold
-      run_rowpipe(pp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx, d_status, st);
-      return;
-    }
     const ThrPlan tp = plan_rowthr(dtype, d_in, p->n, p->num_buckets, p->local_k, p->global_k);
     if (tp.ok) {  // row-resident, row threshold: stage 1 + stage 2 in one warp per row
       run_rowthr(dtype, tp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,
@@ -758,7 +837,7 @@ int atkg_exact_top_k(int dtype, const void* d_in, uint64_t rows, uint64_t n, uin
     if (n > 0xffffffffull + 1) throw_inval("input exceeds the 32-bit index range");
     if (k > n) throw_inval("k must not exceed the input length");
     if (rows == 0) return;
-    (void)ws_bytes;
+    check_ws(ws_bytes, ws_need(ATKG_OP_EXACT, dtype, rows, atkg_params{n, 1, 1, k, 1}));
     char* w = reinterpret_cast<char*>(align_up(reinterpret_cast<uintptr_t>(d_ws)));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (dtype == ATKG_BF16) {
@@ -778,7 +857,7 @@ int atkg_stage1_summary(int dtype, const void* d_slice, uint64_t len, uint64_t i
     const uint64_t B = p->num_buckets;
     if (len % B != 0 || index_offset % B != 0) throw_inval("slice length and offset must be multiples of num_buckets");
     if (index_offset + len > p->n) throw_inval("slice exceeds the row");
-    (void)ws_bytes;
+    check_ws(ws_bytes, ws_need(ATKG_OP_SUMMARY, dtype, 1, atkg_params{len, B, p->local_k, 1, 1}));
     if (!kp_specialised(p->local_k)) throw Unsupported("local_k has no specialised summary kernel");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const S1Plan pl = plan_stage1(dtype, d_slice, 1, len, len, B, p->local_k);
@@ -796,7 +875,7 @@ int atkg_summary_merge_top_k(const uint32_t* d_summaries, uint32_t parts, const 
     validate(*p);
     if (parts == 0) throw_inval("need at least one summary");
     if (!kp_specialised(p->local_k)) throw Unsupported("local_k has no specialised merge kernel");
-    (void)ws_bytes;
+    check_ws(ws_bytes, ws_need(ATKG_OP_MERGE, ATKG_F32, 1, *p));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     char* w = reinterpret_cast<char*>(align_up(reinterpret_cast<uintptr_t>(d_ws)));
     const uint64_t gstride = (uint64_t)p->local_k * p->num_buckets;

@@ -396,10 +396,7 @@ uint32_t fused_nb(const atkg_params& p) {
 // needs the B tile to split into two 8-row-aligned halves (and, for the
 // bucket-complete 3-D box, an even number of stride-rows)
 uint32_t gemm_cg(uint32_t tn, uint32_t S, uint32_t nb) {
-  static const uint32_t forced = [] {
-    const char* e = std::getenv("ATKG_GEMM_CG");
-    return e ? (uint32_t)std::atoi(e) : 0u;
-  }();
+  const uint32_t forced = (uint32_t)opt("gemm_cg", 0);
   const bool pair_ok = (tn / 2) % 8 == 0 && (nb != 1 || S % 16 == 0);
   if (forced == 1 || !pair_ok) return 1;
   return 2;
@@ -409,14 +406,7 @@ template <int CG, int NB, int KP>
 void launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, GemmArgs ga, cudaStream_t st) {
   const size_t smem = gemm_smem_bytes(ga.tn, CG);
   ga.stages = gemm_stages(ga.tn, CG);
-  static bool attr = false;
-  if (!attr) {  // the largest ring any shape of this instantiation asks for
-    int dev = 0, optin = 0;
-    CUDA_OK(cudaGetDevice(&dev));
-    CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    CUDA_OK(cudaFuncSetAttribute(gemm_tc_kernel<CG, NB, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    attr = true;
-  }
+  ensure_smem_fn(gemm_tc_kernel<CG, NB, KP>, smem);
   const uint32_t tiles = ga.m_blocks * ga.n_tiles;
   const uint32_t units = std::min<uint32_t>(tiles, (uint32_t)sm_count() / CG);
   cudaLaunchConfig_t cfg{};
@@ -463,13 +453,10 @@ void run_plain_gemm(const void* x, const void* w_t, uint64_t m, uint64_t kdim, u
 
 // Unfused alternative for shapes the fused epilogue supports (plain GEMM ->
 // grid stage 1 -> stage 2, identical results).  Off by default: no shape has
-// measured faster this way yet.  ATKG_FUSED_PATH=unfused selects it.
-bool small_d_unfused(uint64_t m, uint64_t kdim, const atkg_params& p) {
-  (void)m;
-  (void)kdim;
+// measured faster this way yet.  Option fused_path=1 selects it (tests).
+bool unfused_requested(const atkg_params& p) {
   if (p.local_k > p.n / p.num_buckets) return false;  // grid slots all filled
-  const char* f = std::getenv("ATKG_FUSED_PATH");
-  return f && std::strcmp(f, "unfused") == 0;
+  return opt("fused_path", 0) == 1;
 }
 
 uint64_t fused_cand_bytes(uint64_t m, const atkg_params& p) {
@@ -487,7 +474,7 @@ int atkg_fused_workspace_size(uint64_t m, uint64_t kdim, const atkg_params* p, s
   return guarded([&] {
     if (p == nullptr || bytes == nullptr) throw_inval("null argument");
     validate(*p);
-    if (fused_nb(*p) != 0 && small_d_unfused(m, kdim, *p)) {
+    if (fused_nb(*p) != 0 && unfused_requested(*p)) {
       const uint64_t count = (uint64_t)p->num_buckets * p->local_k;
       size_t s1 = 0;
       if (atkg_workspace_size(ATKG_OP_STAGE1, ATKG_F32, m, p, &s1) != ATKG_OK) throw Inval(atkg_last_error());
@@ -528,7 +515,7 @@ int atkg_fused_gemm_top_k(const void* d_x, const void* d_w_t, uint64_t m, uint64
       if (rc != ATKG_OK) throw Inval(atkg_last_error());
       return;
     }
-    if (small_d_unfused(m, kdim, *p)) {
+    if (unfused_requested(*p)) {
       // write the fp32 scores, then the grid stage 1 + stage 2 (identical results)
       uint8_t* w = static_cast<uint8_t*>(d_ws);
       float* scores = d_scores ? d_scores : reinterpret_cast<float*>(w);

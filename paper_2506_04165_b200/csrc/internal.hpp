@@ -55,7 +55,20 @@ inline void check_launch() {
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
+// SM count of the calling thread's current device (cached per device)
 int sm_count();
+int current_device();
+// raises a kernel's dynamic shared-memory limit to >= bytes on the current
+// device (the attribute is per device; cached per (device, kernel))
+void ensure_smem(const void* kern, size_t bytes);
+template <typename K>
+inline void ensure_smem_fn(K* kern, size_t bytes) { ensure_smem(reinterpret_cast<const void*>(kern), bytes); }
+
+// Path-selection and tuning overrides (atkg_set_option): tests force the
+// rare fallbacks and alternative dispatch paths through these; every
+// default is the measured production choice.  Process-wide.
+uint64_t opt(const char* name, uint64_t dflt);
+
 uint64_t align_up(uint64_t x, uint64_t a = 256);
 uint32_t next_pow2(uint64_t x);
 void validate(const atkg_params& p);
@@ -73,16 +86,6 @@ ThrPlan plan_rowthr(int dtype, const void* in, uint64_t n, uint64_t B, uint32_t 
 uint64_t rowthr_ws_bytes(uint64_t rows, const ThrPlan& tp);
 void run_rowthr(int dtype, const ThrPlan& tp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
                 uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
-
-// persistent row pipeline for bf16 rows in shared memory (rowpipe.cu)
-struct PipePlan {
-  bool ok = false;
-  uint32_t cap = 512, rsel = 1, slot_bytes = 0, scr_words = 0, grid = 1;
-  size_t smem = 0;
-};
-PipePlan plan_rowpipe(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k);
-void run_rowpipe(const PipePlan& pp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
-                 float* ov, uint32_t* oi, uint32_t* status, cudaStream_t st);
 
 // stage 2 by counting-sort ranks for 128 < count <= 1024 (streamthr.cu);
 // false if not applicable

@@ -12,20 +12,11 @@ namespace atkg {
 
 namespace {
 
-uint64_t env_flag(const char* name) {
-  const char* e = std::getenv(name);
-  return e ? std::strtoull(e, nullptr, 10) : 0;
-}
-
 template <int KP, int B>
 void launch(const ThrPlan& tp, const __nv_bfloat16* in, uint64_t rows, uint32_t n, uint32_t k, float* ov,
             uint32_t* oi, uint32_t* status, cudaStream_t st) {
   auto kern = row_threshold_kernel<KP, B>;
-  static size_t attr = 0;
-  if (attr < tp.smem) {
-    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp.smem));
-    attr = tp.smem;
-  }
+  ensure_smem_fn(kern, tp.smem);
   kern<<<(unsigned)rows, B, tp.smem, st>>>(in, n, k, tp.cap, tp.rsel, tp.region, ov, oi, status);
   check_launch();
 }
@@ -34,12 +25,12 @@ void launch(const ThrPlan& tp, const __nv_bfloat16* in, uint64_t rows, uint32_t 
 
 ThrPlan plan_rowthr(int dtype, const void* in, uint64_t n, uint64_t B, uint32_t kp, uint32_t k) {
   ThrPlan tp;
-  if (env_flag("ATKG_NO_ROWTHR")) return tp;
+  if (opt("no_rowthr", 0)) return tp;
   if (dtype != ATKG_BF16 || (kp != 1 && kp != 2 && kp != 4 && kp != 8)) return tp;
   // measured on B200 (C3 shapes): the row threshold wins where the exact
   // per-bucket network of row_resident_kernel is long (K' = 8: 2x); at K' <= 4
-  // that kernel is faster.  ATKG_ROWTHR=1 forces this path (tests).
-  if (kp < 8 && !env_flag("ATKG_ROWTHR")) return tp;
+  // that kernel is faster.  Option rowthr=1 forces this path (tests).
+  if (kp < 8 && !opt("rowthr", 0)) return tp;
   const uint64_t row_bytes = n * 2;
   if (row_bytes > 64 * 1024 || row_bytes % 16 != 0 || reinterpret_cast<uintptr_t>(in) % 16 != 0) return tp;
   // one thread per (word column, row half): B threads
@@ -67,7 +58,7 @@ ThrPlan plan_rowthr(int dtype, const void* in, uint64_t n, uint64_t B, uint32_t 
   const double frac = 1.0 - std::pow(1.0 - q, ns);
   const uint64_t r = (uint64_t)std::ceil((double)B * frac);
   tp.rsel = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(B, r));
-  const uint64_t rr = env_flag("ATKG_ROWTHR_R");
+  const uint64_t rr = opt("rowthr_r", 0);
   if (rr) tp.rsel = (uint32_t)std::min<uint64_t>(B, rr);
   tp.ok = true;
   return tp;

@@ -240,7 +240,7 @@ int atkg_simulate_recall_many(const atkg_params* configs, uint32_t num_configs, 
     // pinned buffer, so pinning stays cheap and generation overlaps the GPU.
     // Rows of n <= 2^16 are generated on the device (synth_distinct_kernel):
     // no host generation, no H2D; larger rows come from host workers.
-    const bool dev_gen = n <= kDeviceSynthMaxN && !std::getenv("ATKG_SIM_HOST_GEN");
+    const bool dev_gen = n <= kDeviceSynthMaxN && !opt("sim_host_gen", 0);
     const uint64_t workers = std::max<uint32_t>(threads, 1);
     const uint64_t batch = dev_gen ? std::min<uint64_t>(runs, 2048)
                                    : std::min<uint64_t>(runs, std::max<uint64_t>(workers, (1ull << 23) / n));

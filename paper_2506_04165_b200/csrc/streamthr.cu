@@ -13,11 +13,6 @@ namespace atkg {
 
 namespace {
 
-uint64_t env_u64(const char* name, uint64_t dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::strtoull(e, nullptr, 10) : dflt;
-}
-
 // E[min(K', X)], X ~ Poisson(lambda)
 double mean_min_poisson(double lambda, uint32_t kp) {
   double p = std::exp(-lambda), cdf = 0.0, m = 0.0;
@@ -41,7 +36,7 @@ void launch_pdl(K kern, unsigned grid, unsigned block, size_t smem, cudaStream_t
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = env_u64("ATKG_NO_PDL", 0) ? 0 : 1;
+  attr[0].val.programmaticStreamSerializationAllowed = opt("no_pdl", 0) ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   CUDA_OK(cudaLaunchKernelEx(&cfg, kern, args));
@@ -51,25 +46,17 @@ void launch_pdl(K kern, unsigned grid, unsigned block, size_t smem, cudaStream_t
 template <typename T, int UNR>
 void launch_stream(const StPlan& sp, const StArgs& a, cudaStream_t st) {
   auto kern = st_stream_kernel<T, UNR>;
-  static size_t attr = 0;
-  if (attr < sp.smem_stream) {
-    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem_stream));
-    attr = sp.smem_stream;
-  }
+  ensure_smem_fn(kern, sp.smem_stream);
   launch_pdl(kern, sp.G, kStNW * 32, sp.smem_stream, st, a);
 }
 
 template <typename T, int KP>
 void launch_finish(const StPlan& sp, uint64_t rows, const StFinArgs& a, cudaStream_t st) {
   auto kern = st_finish_kernel<T, KP>;
-  static size_t attr = 0;
-  if (attr < sp.smem_fin) {
-    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem_fin));
-    attr = sp.smem_fin;
-  }
+  ensure_smem_fn(kern, sp.smem_fin);
   // a few rows (the giant row): one CTA per row is latency-bound, so give it
   // 32 warps; many rows: 8 warps per row, several rows per SM
-  const unsigned threads = rows < 64 ? 1024u : (unsigned)env_u64("ATKG_ST_FIN_THREADS", 256);
+  const unsigned threads = rows < 64 ? 1024u : (unsigned)opt("st_fin_threads", 256);
   launch_pdl(kern, (unsigned)rows, threads, sp.smem_fin, st, a);
 }
 
@@ -78,20 +65,20 @@ void launch_finish(const StPlan& sp, uint64_t rows, const StFinArgs& a, cudaStre
 StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
                       bool for_size) {
   StPlan sp;
-  if (!for_size && env_u64("ATKG_NO_STREAMTHR", 0)) return sp;
+  if (!for_size && opt("no_streamthr", 0)) return sp;
   if (kp != 1 && kp != 2 && kp != 4 && kp != 8) return sp;
   // Many rows with a large K: the per-row finish (rebuild + rank of >= K
   // survivors) outweighs the stream's saving over the exact grid stage 1 +
   // stage 2 (MIPS shape 1024 x 1,000,448, K = 1024, B = 1024, K' = 4:
   // 13.6 -> 6.2 ms per batch after the tcgen05 GEMM).  Sizing keeps the
   // stream's workspace either way.
-  if (!for_size && k >= 1024 && rows >= env_u64("ATKG_STREAMTHR_BIGK_ROWS", 64)) return sp;
+  if (!for_size && k >= 1024 && rows >= opt("streamthr_bigk_rows", 64)) return sp;
   const uint64_t es = dtype == ATKG_BF16 ? 2 : 4;
   const uint64_t ve = 16 / es;
-  if (n < env_u64("ATKG_STREAMTHR_MIN_N", 32768) || n % ve != 0) return sp;
+  if (n < opt("streamthr_min_n", 32768) || n % ve != 0) return sp;
   // rows beyond 2^24 elements (the giant row) do not take the in-kernel exact
   // fallback; a failed row is flagged and rerun on the exact path by the host
-  sp.giant = n > env_u64("ATKG_ST_GIANT_N", 1ull << 24);
+  sp.giant = n > opt("st_giant_n", 1ull << 24);
   if (n > 0xffffffffull) return sp;
   if (reinterpret_cast<uintptr_t>(in) % 16 != 0) return sp;
   const uint64_t filled = std::min<uint64_t>(kp, n / B);
@@ -100,10 +87,10 @@ StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint
   if (sp.vtot >= (1ull << 50)) return sp;
   if (sp.vtot / std::max<uint64_t>(1, (uint64_t)sm_count()) >= (1ull << 31)) return sp;  // 32-bit piece offsets
   // bytes per CTA step = kStNW warps x 32 lanes x UNR 16-byte vectors, UNR in {4, 8}
-  sp.slot_bytes = (uint32_t)env_u64("ATKG_ST_STEP", (uint64_t)kStNW * 4096);
+  sp.slot_bytes = (uint32_t)opt("st_step", (uint64_t)kStNW * 4096);
   if (sp.slot_bytes != (uint32_t)kStNW * 2048 && sp.slot_bytes != (uint32_t)kStNW * 4096) return sp;
   sp.ns = 0;
-  const uint64_t per_sm = env_u64("ATKG_ST_CTAS", 16 / kStNW);
+  const uint64_t per_sm = opt("st_ctas", 16 / kStNW);
   uint64_t G = (uint64_t)sm_count() * per_sm;
   G = std::max<uint64_t>(1, std::min<uint64_t>(G, sp.vtot / 1024));
   sp.psz = (sp.vtot + G - 1) / G;
@@ -166,7 +153,7 @@ void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, u
   a.rfac = sp.rfac;
   a.lfac = sp.lfac;
   a.cfac = sp.cfac;
-  a.warp_sample = (uint32_t)env_u64("ATKG_ST_WARP_SAMPLE", 0);
+  a.warp_sample = (uint32_t)opt("st_warp_sample", 0);
   a.slots = static_cast<uint32_t*>(ws);
   uint32_t* gate = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + (sp.ws_bytes - 256));
   a.gate = sp.giant ? gate : nullptr;
@@ -185,7 +172,7 @@ void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, u
   f.out_v = ov;
   f.out_i = oi;
   f.status = status;
-  f.force_slow = (uint32_t)env_u64("ATKG_ST_FORCE_SLOW", 0);
+  f.force_slow = (uint32_t)opt("st_force_slow", 0);
   f.gate = a.gate;
   g_prof.bracket_begin(st);
   if (dtype == ATKG_BF16) {
@@ -213,10 +200,10 @@ void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, u
 
 bool run_select_ranked(const float* vals, const uint32_t* idx, uint64_t rows, uint64_t count, uint64_t stride,
                        uint32_t k, uint64_t limit, float* ov, uint32_t* oi, uint32_t* status, cudaStream_t st) {
-  if (env_u64("ATKG_NO_RANK_SELECT", 0) || count <= 128 || count > 1024) return false;
+  if (opt("no_rank_select", 0) || count <= 128 || count > 1024) return false;
   uint32_t P = 2;
   while (P < count) P <<= 1;
-  const unsigned threads = (unsigned)env_u64("ATKG_S2_THREADS", 128);
+  const unsigned threads = (unsigned)opt("s2_threads", 128);
   stage2_rank_kernel<<<(unsigned)rows, threads, (size_t)P * 16, st>>>(vals, idx, (uint32_t)count, stride, k, limit,
                                                                        P, ov, oi, status);
   check_launch();

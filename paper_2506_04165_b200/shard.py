@@ -45,9 +45,17 @@ def slice_bounds(n: int, num_buckets: int, world: int, rank: int, align: int = G
 class ShardedTopK:
     """Approximate top-K of one row sharded over the ranks of `group`.
 
-    `summarize(slice, offset, params)` -> int32 tensor of summary_words(params)
-    `merge(summaries [world, words], params)` -> (values, indices)
-    default to the device kernels (atkg_stage1_summary / atkg_summary_merge_top_k).
+    `summarize(slice, offset, params, status)` -> int32 tensor of
+    summary_words(params); ORs the NaN flag into the int32 `status` tensor.
+    `merge(summaries [world, words], params)` -> (values, indices).
+    Both default to the device kernels (atkg_stage1_summary /
+    atkg_summary_merge_top_k).
+
+    NaN: every rank's NaN flag travels as one extra word of its gathered
+    summary, so all ranks see the same verdict with no extra collective --
+    they all raise "input contains NaN" (topk.cpp:22-28), or with a caller
+    `status` tensor all OR the flag into it, instead of one rank raising
+    before the all-gather while the others wait in it.
     """
 
     def __init__(self, params: AlgoParams, group=None, summarize=None, merge=None):
@@ -59,10 +67,12 @@ class ShardedTopK:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.words = summary_words(params)
-        self.summarize = summarize or (lambda x, off, p: stage1_summary_device(x, off, p, status=self._status))
-        self.merge = merge or (lambda s, p: summary_merge_top_k_device(s, p, status=self._status))
-        self._status = None
+        self.summarize = summarize or (lambda x, off, p, st: stage1_summary_device(x, off, p, out=self._out, status=st))
+        self.merge = merge or (lambda s, p: summary_merge_top_k_device(s, p, status=self._merge_status))
+        self._send = None
         self._gathered = None
+        self._out = None
+        self._merge_status = None
 
     def bounds(self, rank: int | None = None) -> tuple[int, int]:
         return slice_bounds(self.params.n, self.params.num_buckets, self.world,
@@ -75,9 +85,24 @@ class ShardedTopK:
         start, length = self.bounds()
         if x_slice.numel() != length:
             raise ValueError(f"rank {self.rank} slice must hold {length} elements")
-        self._status = status
-        summ = self.summarize(x_slice, start, self.params)
-        if self._gathered is None or self._gathered.device != summ.device:
-            self._gathered = torch.empty(self.world * self.words, dtype=summ.dtype, device=summ.device)
-        self.dist.all_gather_into_tensor(self._gathered, summ, group=self.group)
-        return self.merge(self._gathered.view(self.world, self.words), self.params)
+        w = self.words
+        if self._send is None or self._send.device != x_slice.device:
+            self._send = torch.empty(w + 1, dtype=torch.int32, device=x_slice.device)
+            self._gathered = torch.empty(self.world * (w + 1), dtype=torch.int32, device=x_slice.device)
+        self._out = self._send[:w]
+        flag = self._send[w:]
+        flag.zero_()
+        summ = self.summarize(x_slice, start, self.params, flag)
+        if summ.data_ptr() != self._send.data_ptr():
+            self._send[:w].copy_(summ.view(torch.int32).reshape(-1))
+        self.dist.all_gather_into_tensor(self._gathered, self._send, group=self.group)
+        g = self._gathered.view(self.world, w + 1)
+        flags = g[:, w]
+        if status is None:
+            if int(flags.max().item()) & 1:
+                raise ValueError("input contains NaN")
+            self._merge_status = None
+        else:
+            status.bitwise_or_(flags.amax().view(1).to(status.dtype))
+            self._merge_status = status
+        return self.merge(g[:, :w].contiguous(), self.params)

@@ -16,6 +16,7 @@ bit-identical for n < 2^31.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -111,25 +112,32 @@ _approx_plan_cache: dict = {}
 
 
 def workspace(nbytes: int, device) -> "torch.Tensor":
-    """Caller-supplied scratch (include/atkg.h): cached per device, grow-only."""
-    key = (device.index if hasattr(device, "index") else device)
+    """Caller-supplied scratch (include/atkg.h), cached per (device, stream):
+    calls on different streams never share scratch (a buffer is only reused
+    by work ordered after it on the same stream)."""
+    dev = device.index if hasattr(device, "index") and device.index is not None else torch.cuda.current_device()
+    stream = torch.cuda.current_stream(dev)
+    key = (dev, stream.cuda_stream)
     buf = _ws_cache.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        # allocated on `stream`: the caching allocator hands a freed block
+        # back only to later work on that same stream
+        buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=torch.device("cuda", dev))
         _ws_cache[key] = buf
     return buf
 
 
-_cur_dev = [None]
+_tls = threading.local()
 
 
 def _stream_ptr(device) -> int:
     """Current torch stream of `device`; also points the library's CUDA
-    runtime at that device (it keeps its own per-thread device state)."""
+    runtime at that device (its device state is per host thread, so the
+    cache is too)."""
     idx = device.index if device.index is not None else torch.cuda.current_device()
-    if _cur_dev[0] != idx:
+    if getattr(_tls, "dev", None) != idx:
         check(lib.atkg_set_device(idx))
-        _cur_dev[0] = idx
+        _tls.dev = idx
     return torch.cuda.current_stream(device).cuda_stream
 
 

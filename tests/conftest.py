@@ -90,3 +90,20 @@ def load_emu(path=EMU_LIB):
 @pytest.fixture(scope="session")
 def emu():
     return load_emu(build_emu())
+
+
+@pytest.fixture
+def opts():
+    """opts(name, value): a library path-selection override (atkg_set_option)
+    for the duration of one test."""
+    from paper_2506_04165_b200 import _lib
+    touched = {}
+
+    def set_(name, value):
+        if name not in touched:
+            touched[name] = _lib.lib.atkg_get_option(name.encode(), 2**64 - 1)
+        _lib.set_option(name, value)
+
+    yield set_
+    for name, prev in touched.items():
+        _lib.set_option(name, None if prev == 2**64 - 1 else prev)

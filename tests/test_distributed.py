@@ -53,11 +53,12 @@ def _worker(rank, world, port, emu_path, n, B, kp, k, seed, out_dir):
         port_be = O.port()
         p = AlgoParams(n, B, kp, k, 1)
 
-        def summarize(x, offset, params):
+        def summarize(x, offset, params, status):
             xs = np.ascontiguousarray(x.numpy(), np.float32)
             words = np.empty((2 * kp + 2) * B, np.uint32)
             nan = C.c_uint32()
             assert emu.emu_slice_summary(xs, xs.size, offset, B, kp, words, C.byref(nan)) == 0
+            status |= int(nan.value != 0)
             return torch.from_numpy(words.view(np.int32))
 
         def merge(summaries, params):

@@ -143,14 +143,14 @@ def test_c4_full_size(cuda, ref):
 
 
 @pytest.mark.parametrize("m,kd,n,B,kp,k,lane", [FUSED[2], FUSED[4], FUSED[7]])
-def test_unfused_alternative_identical(cuda, port, monkeypatch, m, kd, n, B, kp, k, lane):
-    """ATKG_FUSED_PATH=unfused (plain GEMM -> grid stage 1 -> stage 2) returns
+def test_unfused_alternative_identical(cuda, port, opts, m, kd, n, B, kp, k, lane):
+    """Option fused_path=1 (plain GEMM -> grid stage 1 -> stage 2) returns
     the fused epilogue's results bit for bit."""
     x, w = operands(m, kd, n, 17 + m, cuda)
     p = atk.AlgoParams(n, B, kp, k, lane)
-    monkeypatch.delenv("ATKG_FUSED_PATH", raising=False)
+    opts("fused_path", 0)
     fv, fi = T.fused_gemm_top_k_device(x, w, p)
-    monkeypatch.setenv("ATKG_FUSED_PATH", "unfused")
+    opts("fused_path", 1)
     scores = torch.empty((m, n), dtype=torch.float32, device=cuda)
     uv, ui = T.fused_gemm_top_k_device(x, w, p, scores=scores)
     uv2, ui2 = T.fused_gemm_top_k_device(x, w, p)

@@ -6,9 +6,8 @@ Every case is compared bit for bit with the reference library
 (oracle/_ref, approx_top_k_batch) -- including rows that defeat the
 threshold guess (the exact slow path), heavy ties, -inf rows, and the
 counting-sort / bitonic switch -- and with the previous row-resident kernel
-(ATKG_NO_ROWTHR=1), which computes the full grid.
+(option no_rowthr=1), which computes the full grid.
 """
-import os
 
 import numpy as np
 import pytest
@@ -21,9 +20,9 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(autouse=True)
-def _force_rowthr(monkeypatch):
+def _force_rowthr(opts):
     """The planner picks this path for K' >= 8 only; force it for every K'."""
-    monkeypatch.setenv("ATKG_ROWTHR", "1")
+    opts("rowthr", 1)
 
 
 def bits(a):
@@ -131,11 +130,8 @@ def test_rowthr_ties_vs_old_kernel(cuda, ref, levels):
     x = rng.integers(-levels, levels + 1, size=(128, 14336)).astype(np.float32) / 4.0
     v, i = check(ref, cuda, x, "bf16", 128, 4, 287)
     xd, _ = dev_input(x, "bf16", cuda)
-    os.environ["ATKG_NO_ROWTHR"] = "1"
-    try:
+    with atk._lib.option("no_rowthr", 1):
         v2, i2 = atk.approx_top_k_device(xd, atk.AlgoParams(14336, 128, 4, 287))
-    finally:
-        del os.environ["ATKG_NO_ROWTHR"]
     assert np.array_equal(bits(v), bits(v2)) and np.array_equal(u32(i), u32(i2))
 
 

@@ -9,7 +9,6 @@ rows at several shapes and both dtypes, rows that defeat the threshold
 (ramps, -inf rows, all-equal rows, +-0, +inf, quantised ties), row/piece
 boundary layouts, the forced exact fallback, and NaN rejection.
 """
-import os
 
 import numpy as np
 import pytest
@@ -75,8 +74,8 @@ def test_streamthr_normal_vs_reference(cuda, ref, dtype, rows, n, B, kp, k):
 
 
 @pytest.mark.parametrize("dtype,rows,n,B,kp,k", [s for s in SHAPES if s[1] >= 3 and s[2] <= 262144])
-def test_streamthr_forced_fallback(cuda, ref, monkeypatch, dtype, rows, n, B, kp, k):
-    monkeypatch.setenv("ATKG_ST_FORCE_SLOW", "1")
+def test_streamthr_forced_fallback(cuda, ref, opts, dtype, rows, n, B, kp, k):
+    opts("st_force_slow", 1)
     rng = np.random.default_rng(n + B + kp + k)
     x = rng.standard_normal((min(rows, 4), n)).astype(np.float32)
     check(ref, cuda, x, dtype, B, kp, k)
@@ -128,26 +127,23 @@ def test_streamthr_nan_flag(cuda):
 
 
 def test_streamthr_matches_previous_path(cuda):
-    """Same answers as the exact-summary streaming path (ATKG_NO_STREAMTHR=1)."""
+    """Same answers as the exact-summary streaming path (option no_streamthr=1)."""
     x = np.random.default_rng(5).standard_normal((32, 262144)).astype(np.float32)
     xd = torch.from_numpy(x).to(cuda)
     p = atk.AlgoParams(262144, 128, 2, 64)
     v, i = atk.approx_top_k_device(xd, p)
-    os.environ["ATKG_NO_STREAMTHR"] = "1"
-    try:
+    with atk._lib.option("no_streamthr", 1):
         v2, i2 = atk.approx_top_k_device(xd, p)
-    finally:
-        del os.environ["ATKG_NO_STREAMTHR"]
     assert np.array_equal(bits(v), bits(v2)) and np.array_equal(u32(i), u32(i2))
 
 
 @pytest.mark.parametrize("force", [False, True])
-def test_streamthr_giant_row_gate(cuda, ref, monkeypatch, force):
+def test_streamthr_giant_row_gate(cuda, ref, opts, force):
     """Giant-row mode (no in-kernel fallback): a failed row is flagged and the
     host reruns the exact path; both outcomes match the reference."""
-    monkeypatch.setenv("ATKG_ST_GIANT_N", "65536")
+    opts("st_giant_n", 65536)
     if force:
-        monkeypatch.setenv("ATKG_ST_FORCE_SLOW", "1")
+        opts("st_force_slow", 1)
     rng = np.random.default_rng(77)
     x = rng.standard_normal((2, 1 << 21)).astype(np.float32)
     check(ref, cuda, x, "f32", 256, 8, 1024)

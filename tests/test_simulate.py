@@ -119,12 +119,12 @@ def test_synth_distinct_device_limits(cuda):
 
 
 @pytest.mark.gpu
-def test_simulate_device_and_host_generation_agree(cuda, ref, monkeypatch):
+def test_simulate_device_and_host_generation_agree(cuda, ref, opts):
     import paper_2506_04165_b200 as atk
     configs = [atk.AlgoParams(n=65536, num_buckets=256, local_k=2, global_k=64),
                atk.AlgoParams(n=65536, num_buckets=512, local_k=1, global_k=128)]
     dev = atk.simulate_recall_many(configs, 300, 31, device=cuda)
-    monkeypatch.setenv("ATKG_SIM_HOST_GEN", "1")
+    opts("sim_host_gen", 1)
     host = atk.simulate_recall_many(configs, 300, 31, device=cuda)
     mean, sd = ref_simulate(ref.lib, configs, 300, 31)
     for c in range(2):
