@@ -650,6 +650,8 @@ size_t ws_need_uncached(int op, int dtype, uint64_t rows, const atkg_params& pr)
         if (tp.ok) b = std::max<size_t>(b, rowthr_ws_bytes(rows, tp));
         const StPlan sp = plan_streamthr(dtype, in, rows, p->n, p->num_buckets, p->local_k, p->global_k, true);
         if (sp.ok) b = std::max<size_t>(b, sp.ws_bytes);
+        const SrPlan srp = plan_short(dtype, in, rows, p->n, p->num_buckets, p->local_k, p->global_k, true);
+        if (srp.ok) b = std::max<size_t>(b, srp.ws_bytes);
         break;
       }
       case ATKG_OP_SELECT:
@@ -805,6 +807,12 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     float* gv = reinterpret_cast<float*>(w);
     uint32_t* gi = reinterpret_cast<uint32_t*>(w + rows * gstride * 4);
     w += grid_bytes(rows, *p);
+    const SrPlan srp = plan_short(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
+    if (srp.ok) {  // rows in shared memory, guaranteed row threshold (shortrow.cuh)
+      run_short(dtype, srp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,
+                reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(d_ws))), d_status, st);
+      return;
+    }
     const ThrPlan tp = plan_rowthr(dtype, d_in, p->n, p->num_buckets, p->local_k, p->global_k);
     if (tp.ok) {  // row-resident, row threshold: stage 1 + stage 2 in one warp per row
       run_rowthr(dtype, tp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,

@@ -87,6 +87,18 @@ uint64_t rowthr_ws_bytes(uint64_t rows, const ThrPlan& tp);
 void run_rowthr(int dtype, const ThrPlan& tp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
                 uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
 
+// short rows held in shared memory, guaranteed row threshold (shortrow.cu)
+struct SrPlan {
+  bool ok = false;
+  uint32_t wg = 1, cap = 0, slot_bytes = 0, P = 0, sub_shift = 0, grid = 0, per_sm = 0;
+  size_t smem = 0;
+  uint64_t ws_bytes = 0;
+};
+SrPlan plan_short(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
+                  bool for_size = false);
+void run_short(int dtype, const SrPlan& sp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
+               uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
+
 // stage 2 by counting-sort ranks for 128 < count <= 1024 (streamthr.cu);
 // false if not applicable
 bool run_select_ranked(const float* vals, const uint32_t* idx, uint64_t rows, uint64_t count, uint64_t stride,

@@ -63,28 +63,6 @@ constexpr uint32_t kStBadCount = 0xffffffffu;
 constexpr uint32_t kStMaxRowPieces = 2048;  // pieces one row may span (host-checked)
 constexpr uint32_t kStFewSlots = 3;         // finish: one-round-trip gather up to this many slots
 
-// ascending order key of a non-NaN float, -0 == +0
-__device__ __forceinline__ uint32_t st_okey(float x) {
-  uint32_t u = __float_as_uint(x);
-  if (u == 0x80000000u) u = 0;
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-__device__ __forceinline__ float st_oval(uint32_t k) {
-  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
-}
-constexpr uint32_t kStKeyNegInf = 0x007fffffu;  // st_okey(-inf)
-
-__device__ __forceinline__ float fmax_nan(float a, float b) {
-  float r;
-  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ uint32_t bmax_nan(uint32_t a, uint32_t b) {
-  uint32_t r;
-  asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
-  return r;
-}
-
 struct StArgs {
   const void* in;
   uint64_t n;          // row length

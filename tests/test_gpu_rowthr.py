@@ -21,8 +21,10 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(autouse=True)
 def _force_rowthr(opts):
-    """The planner picks this path for K' >= 8 only; force it for every K'."""
+    """The planner picks this path for K' >= 8 only (and only when the
+    short-row kernel does not apply); force it for every K'."""
     opts("rowthr", 1)
+    opts("no_short", 1)
 
 
 def bits(a):
