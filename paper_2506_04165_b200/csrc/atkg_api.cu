@@ -650,6 +650,8 @@ size_t ws_need_uncached(int op, int dtype, uint64_t rows, const atkg_params& pr)
         if (tp.ok) b = std::max<size_t>(b, rowthr_ws_bytes(rows, tp));
         const StPlan sp = plan_streamthr(dtype, in, rows, p->n, p->num_buckets, p->local_k, p->global_k, true);
         if (sp.ok) b = std::max<size_t>(b, sp.ws_bytes);
+        const RwPlan rwp = plan_rowwarp(dtype, in, rows, p->n, p->num_buckets, p->local_k, p->global_k, true);
+        if (rwp.ok) b = std::max<size_t>(b, rwp.ws_bytes);
         const SrPlan srp = plan_short(dtype, in, rows, p->n, p->num_buckets, p->local_k, p->global_k, true);
         if (srp.ok) b = std::max<size_t>(b, srp.ws_bytes);
         break;
@@ -807,7 +809,20 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     float* gv = reinterpret_cast<float*>(w);
     uint32_t* gi = reinterpret_cast<uint32_t*>(w + rows * gstride * 4);
     w += grid_bytes(rows, *p);
-    const SrPlan srp = plan_short(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
+    // the guaranteed-threshold row kernels (rowwarp.cuh, shortrow.cuh) are
+    // bit-exact but not yet faster than row_resident_kernel where that one
+    // applies; they run where it does not, or when selected
+    const RowPlan rrp = plan_rowres(dtype, d_in, p->n, p->num_buckets, p->local_k);
+    const bool row_new = !rrp.ok || opt("short", 0) || opt("rowwarp", 0);
+    const RwPlan rwp = row_new ? plan_rowwarp(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k)
+                               : RwPlan{};
+    if (rwp.ok) {  // one warp per row in shared memory, guaranteed row threshold (rowwarp.cuh)
+      run_rowwarp(rwp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,
+                  reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(d_ws))), d_status, st);
+      return;
+    }
+    const SrPlan srp = row_new ? plan_short(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k)
+                               : SrPlan{};
     if (srp.ok) {  // rows in shared memory, guaranteed row threshold (shortrow.cuh)
       run_short(dtype, srp, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx,
                 reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(d_ws))), d_status, st);

@@ -90,7 +90,7 @@ void run_rowthr(int dtype, const ThrPlan& tp, const void* in, uint64_t rows, uin
 // short rows held in shared memory, guaranteed row threshold (shortrow.cu)
 struct SrPlan {
   bool ok = false;
-  uint32_t wg = 1, cap = 0, slot_bytes = 0, P = 0, sub_shift = 0, grid = 0, per_sm = 0;
+  uint32_t npart = 1, pl = 1, cap = 0, slot_bytes = 0, P = 0, sub_shift = 0, grid = 0, per_sm = 0;
   size_t smem = 0;
   uint64_t ws_bytes = 0;
 };
@@ -98,6 +98,18 @@ SrPlan plan_short(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t
                   bool for_size = false);
 void run_short(int dtype, const SrPlan& sp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
                uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
+
+// one warp per bf16 row held in shared memory (rowwarp.cu)
+struct RwPlan {
+  bool ok = false;
+  uint32_t cpl = 1, w = 4, cap = 0, P = 0, slot_bytes = 0, sub_shift = 0, grid = 0;
+  size_t smem = 0;
+  uint64_t ws_bytes = 0;
+};
+RwPlan plan_rowwarp(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
+                    bool for_size = false);
+void run_rowwarp(const RwPlan& rp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
+                 float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
 
 // stage 2 by counting-sort ranks for 128 < count <= 1024 (streamthr.cu);
 // false if not applicable

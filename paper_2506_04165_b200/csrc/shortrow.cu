@@ -51,7 +51,7 @@ void sr_launch(const SrPlan& sp, const SrArgs& a, cudaStream_t st) {
 SrPlan plan_short(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
                   bool for_size) {
   SrPlan sp;
-  if (!for_size && (opt("no_short", 0) || !opt("short", 0))) return sp;  // opt-in while it is slower
+  if (!for_size && opt("no_short", 0)) return sp;
   if (dtype != ATKG_BF16 || (kp != 1 && kp != 2 && kp != 4 && kp != 8)) return sp;
   const uint64_t row_bytes = n * 2;
   // rows that fit a shared-memory slot twice over, 16-byte aligned for TMA
@@ -60,22 +60,28 @@ SrPlan plan_short(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t
   if (B % 4 != 0 || n % B != 0) return sp;
   const uint64_t S = n / B;
   if (S < kp) return sp;  // fewer stride-rows than K': every element is a candidate
+  // parts of <= 32 stride-rows per group, more of them while the units do
+  // not cover the CTA
   const uint64_t gl = (S + kp - 1) / kp;
-  sp.wg = (uint32_t)((gl + 31) / 32);
-  if ((uint64_t)kp * sp.wg > kSrMaxWords) return sp;
-  // candidates of a fast-path row: ~1.5 K for i.i.d. rows; rows with more
-  // (heavy ties at L) take the exact path
+  uint64_t npart = (gl + 31) / 32;
+  while ((B / 4) * kp * npart < (uint64_t)kSrThreads && npart * 2 <= gl && kp * npart * 2 <= kSrMaxWords) npart *= 2;
+  if (kp * npart > kSrMaxWords) return sp;
+  sp.npart = (uint32_t)npart;
+  sp.pl = (uint32_t)((gl + npart - 1) / npart);
+  // candidates: M <= B * K'; i.i.d. rows give ~1.4 K, rows with more (heavy
+  // ties at L) take the exact path
   uint64_t cap = 512;
   while (cap < std::min<uint64_t>(B * kp, 2 * (uint64_t)k + 256)) cap <<= 1;
+  if (cap > 65536) return sp;
   sp.cap = (uint32_t)cap;
   uint64_t P = 2;
   while (P < B * kp) P <<= 1;
   sp.P = (uint32_t)P;
-  // the emit's scratch (tmp[M] | start[1028] | cur[1024]) reuses the dead row slot
-  sp.slot_bytes = (uint32_t)align_up(std::max<uint64_t>(row_bytes, (cap + 2 * kThrNB + 8) * 4), 128);
+  // stage-2 scratch in the dead row slot: keys[2 cap] | emit scratch
+  sp.slot_bytes = (uint32_t)align_up(std::max<uint64_t>(row_bytes, (2 * cap + 2 * kThrNB + 64) * 4), 128);
   sp.sub_shift = 0;
   while ((n - 1) >> sp.sub_shift >= 4) ++sp.sub_shift;
-  sp.smem = sr_smem_bytes(sp.slot_bytes, sp.cap, kp, sp.wg, (uint32_t)B);
+  sp.smem = sr_smem_bytes(sp.slot_bytes, sp.cap, kp, sp.npart, (uint32_t)B);
   bool fit = false;
   switch (kp) {
     case 1: fit = sr_fit<1>(sp); break;
@@ -101,7 +107,8 @@ void run_short(int dtype, const SrPlan& sp, const void* in, uint64_t rows, uint6
   a.S = (uint32_t)(n / B);
   a.k = k;
   a.cps = (uint32_t)(B / 4);
-  a.wg = sp.wg;
+  a.npart = sp.npart;
+  a.pl = sp.pl;
   a.cap = sp.cap;
   a.slot_bytes = sp.slot_bytes;
   a.row_bytes = (uint32_t)(n * 2);

@@ -1,6 +1,6 @@
-"""short_row_kernel (csrc/shortrow.cuh): approx_top_k for rows held in shared
-memory with the guaranteed row threshold (K-th largest of the B*K' group
-maxima).  Bit-exact against the reference library (oracle/_ref, the
+"""row_warp_kernel (csrc/rowwarp.cuh) and short_row_kernel (csrc/shortrow.cuh):
+approx_top_k for bf16 rows held in shared memory with the guaranteed row
+threshold (K-th largest of the B*K' group maxima).  Bit-exact against the reference library (oracle/_ref, the
 unmodified atk core: approx_top_k_batch, topk.cpp:238-273) on the C3 shape,
 its K' sweep (BASELINE configs[2]), small and odd shapes,
 rows built to hit every rare branch (crowded buckets, heavy ties, the exact
@@ -15,9 +15,16 @@ from paper_2506_04165_b200 import data  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True)
-def _short_on(opts):
-    opts("short", 1)
+@pytest.fixture(autouse=True, params=["rowwarp", "short"])
+def kernel_path(request, opts):
+    """Every test runs on the one-warp-per-row kernel (rowwarp.cuh, B in
+    {128, 256, 512}) and on the CTA-per-row kernel (shortrow.cuh); shapes a
+    kernel does not take fall through to the other row kernels."""
+    if request.param == "short":
+        opts("short", 1)
+    else:
+        opts("rowwarp", 1)
+    return request.param
 
 
 def bits(a):
@@ -63,6 +70,13 @@ SHAPES = [  # dtype, n, B, kp, k
     ("bf16", 4096, 4, 2, 8),        # tiny B
     ("bf16", 1000, 8, 4, 30),       # rows of 2000 B (16-byte multiple), 125 stride-rows
     ("bf16", 24576, 96, 2, 150),    # 256 stride-rows: masks over 8 blocks; B not a power of 2
+    ("bf16", 8192, 128, 4, 287),    # 64 stride-rows: two mask words
+    ("bf16", 4096, 128, 2, 100),    # 32 stride-rows: one mask word
+    ("bf16", 16384, 256, 4, 400),   # 64 stride-rows, 2 chunk columns per lane
+    ("bf16", 8192, 512, 1, 200),    # 16 stride-rows, 4 chunk columns per lane
+    ("bf16", 14336, 128, 4, 1),     # K = 1
+    ("bf16", 14336, 128, 8, 1024),  # K = B*K'
+    ("bf16", 1920, 128, 8, 300),    # 15 stride-rows: groups of one or two rows
     ("f32", 4096, 128, 4, 100),
     ("f32", 8192, 64, 2, 100),
     ("f32", 2048, 32, 8, 200),
@@ -117,6 +131,7 @@ def test_short_ties_vs_reference(cuda, ref, levels, kp, B):
                                             ("bf16", 14336, 7168, 1, 287), ("f32", 4096, 128, 8, 100)])
 def test_short_forced_exact_path(cuda, ref, opts, dtype, n, B, kp, k):
     opts("short_force_slow", 1)
+    opts("rowwarp_force_slow", 1)
     x = np.random.default_rng(5).standard_normal((40, n)).astype(np.float32)
     x[3] = np.round(x[3] * 2)
     x[4] = -np.inf

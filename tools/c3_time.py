@@ -34,16 +34,18 @@ def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     new_only = "--new-only" in sys.argv
     which = [tuple(map(int, a.split("/"))) for a in args] or SWEEP
+    atk._lib.set_option("short", 1)  # the short-row kernel (opt-in while under development)
     for kp, b in which:
         p = atk.AlgoParams(n, b, kp, k)
         t_new = timeit(lambda: atk.approx_top_k_device(x, p, status=st, out=out))
         if "--probe" in sys.argv:
-            with atk._lib.option("short_probe", 1):
-                t_probe = timeit(lambda: atk.approx_top_k_device(x, p, status=st, out=out))
-            print(f"K'={kp} B={b}: row pipeline alone {t_probe:7.1f} us", flush=True)
+            for pr, what in [(1, "row pipeline alone"), (2, "+ pass 1 + select"), (3, "+ pass 2"), (4, "+ collect")]:
+                with atk._lib.option("short_probe", pr):
+                    t_probe = timeit(lambda: atk.approx_top_k_device(x, p, status=st, out=out))
+                print(f"K'={kp} B={b}: {what:22s} {t_probe:7.1f} us", flush=True)
         t_old = float("nan")
         if not new_only:
-            with atk._lib.option("no_short", 1):
+            with atk._lib.option("short", 0):
                 t_old = timeit(lambda: atk.approx_top_k_device(x, p, status=st, out=out), iters=10)
         atk.check_status(st)
         gbs = rows * n * 2 / (t_new * 1e-6) / 1e9
