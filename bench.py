@@ -1,7 +1,7 @@
 """Benchmark of the B200 two-stage approximate top-k hot path (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C2]
+                    [--config C2] [--weak] [--sweep]
 
 Workload (default; BASELINE.json configs[1], the config the metric is quoted on):
   C2 "LM-logit rows": fp32 [256, 262144] i.i.d. N(0,1) (seeded, synthetic),
@@ -10,29 +10,36 @@ Workload (default; BASELINE.json configs[1], the config the metric is quoted on)
 A step = approx top-K (stage 1 + stage 2) over the whole batch.
 Other configs (--config): C1 (oracle case), C3 (bf16 [8192, 14336]), C4 (the
 fused tcgen05 GEMM + stage-1 epilogue: a step = scores + top-K of 8192 x 14336,
-roofline against the bf16 tensor-core peak), C5 (one 2^30 row; at N > 1 the
-row is sliced across ranks and the stage-1 summaries are all-gathered over
-NCCL: fixed total work, "scaling": "strong").
+roofline against the bf16 tensor-core peak), C5 (one 2^30 row).
 
   value  whole-job elements/s with inputs already resident in HBM (device
-         API, CUDA events on the launching stream, max over ranks).  The
-         input (268 MB per GPU) is larger than the 126 MB L2, so no flush is
-         needed between steps.
-  e2e    the same metric through the host-buffer C ABI
-         (atkg_approx_top_k_host): pinned host rows -> device -> top-K ->
-         host, every step.
-  roofline  the stage-1 streaming kernel (the dominant kernel): algorithmic
-         bytes per launch (rows*n*4 + rows*B*K'*8) / its live
-         CUDA-event duration inside the timed steps, against the measured HBM
-         copy bandwidth (MEASURED_PEAKS.json).
+         API, CUDA events on the launching stream, max over ranks).  Every
+         input is larger than the 126 MB L2 except C1's 2 MB (a parity-size
+         config, not a bandwidth measurement).
+  e2e    the same metric through the public API with host buffers: the f32
+         configs through the host-buffer C ABI (atkg_approx_top_k_host,
+         pinned host rows -> device -> top-K -> host every step), bf16 rows
+         through the device API with pinned H2D / D2H copies in the region.
+  roofline  the dominant kernel: algorithmic bytes (or FLOPs) per launch /
+         its live CUDA-event duration inside the timed steps, against the
+         measured peaks (MEASURED_PEAKS.json).
   cpu_baseline  the reference library (oracle/_ref: the unmodified atk core
-         compiled from /root/reference) approx_top_k_batch with all host
-         threads, on the same bytes, rank 0 at N=1.
+         compiled from /root/reference) on the same bytes, rank 0 at N=1.
 
-N>1 (torchrun): C1-C4 -- every rank runs its own batch (rows sharded across
-GPUs, no data-path collective), so per-GPU work is fixed: "scaling": "weak".
-C5 -- one row, sliced: "scaling": "strong".
---impl reference runs the reference CPU implementation on rank 0 only.
+Multi-GPU (one process per GPU; `--gpus N` without torchrun re-launches under
+torchrun): the BASELINE batch is SPLIT across the ranks -- C1-C4: rows/N rows
+per rank (C4: x rows, W replicated), the top-K of every rank all-gathered to
+every rank inside the timed region; C5: the row sliced, stage-1 summaries
+all-gathered (shard.ShardedTopK).  Total work is fixed: "scaling": "strong".
+`--weak` gives every rank its own full batch instead.  At N > 1 rank 0 checks
+that the gathered results equal one GPU's run over the whole batch (the
+reference's results do not depend on how rows are split, topk.cpp:260-273).
+
+--impl reference runs the reference CPU implementation (oracle/_ref) on rank
+0 only, without loading the product library: planning through the
+reference's select_parameters and inputs from the oracle's statement of the
+input convention (byte-identical, tests/test_oracle.py).
+--sweep (C3) prints one line per K' sweep point (r = 0.95 and 0.99).
 """
 from __future__ import annotations
 
@@ -65,30 +72,81 @@ CONFIGS = {
     "C5": dict(rows=1, n=1 << 30, k=1024, target=0.95, kps=(8,), dtype="f32", seed="C5", kind="giant",
                label="single giant row fp32 [1, 2^30], K=1024, K'=8, planner r=0.95"),
 }
+# per-config input seeds (the same table as paper_2506_04165_b200/data.py; a
+# copy so the reference arm never imports the product package)
+SEEDS = {"C1": 0, "C2": 2, "C3": 3, "C4x": 4, "C4w": 5, "C5": 6}
+GEN_BLOCK = 65536
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def plan(cfg):
+def metric_name():
+    return "approx top-K Gelem/s & HBM GB/s vs ~8 TB/s roofline at matched expected recall"
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# planning and inputs: product library (ours) or oracle (reference arm)
+# ---------------------------------------------------------------------------
+def plan(cfg, reference=False, target=None, kps=None):
+    """(K', B, expected recall) of the config (planner.cpp:79-147)."""
+    target = cfg.get("target") if target is None else target
+    kps = cfg.get("kps") if kps is None else kps
+    if reference:
+        from oracle import pyoracle as O
+        be = O.ref() if O.ref_available() else O.port()
+        if "fixed" in cfg:
+            kp, b = cfg["fixed"]
+            return kp, b, be.exact_expected_recall(cfg["n"], b, kp, cfg["k"])
+        pl = be.select_parameters(cfg["n"], cfg["k"], target, list(kps), 128, 0)
+        return pl.local_k, pl.num_buckets, pl.recall
     import paper_2506_04165_b200 as atk
     if "fixed" in cfg:
         kp, b = cfg["fixed"]
-        rec = atk.exact_expected_recall(atk.AlgoParams(cfg["n"], b, kp, cfg["k"])).value
-        return kp, b, rec
-    r = atk.select_parameters(atk.PlanRequest(cfg["n"], cfg["k"], cfg["target"], list(cfg["kps"]), 128, 0))
+        return kp, b, atk.exact_expected_recall(atk.AlgoParams(cfg["n"], b, kp, cfg["k"])).value
+    r = atk.select_parameters(atk.PlanRequest(cfg["n"], cfg["k"], target, list(kps), 128, 0))
     return r.local_k, r.num_buckets, r.estimated_recall.value
 
 
-def make_rows(cfg, rank):
-    """Host rows (fp32, or bf16 bits + fp32 upcast) for this rank."""
+def normal_f32(seed, start, count, std=1.0, reference=False):
+    """Elements [start, start + count) of the seeded N(0, std) stream."""
+    if reference:
+        from oracle import pyoracle as O
+        return O.normal_f32(seed, start, count, 0.0, std)
     from paper_2506_04165_b200 import data
-    seed = data.SEEDS[cfg["seed"]] + 1000 * rank
+    return data.normal_f32_range(seed, start, count, std=std)
+
+
+def to_bf16(x, reference=False):
+    """(bf16 bits, exact fp32 values)."""
+    if reference:
+        from oracle import pyoracle as O
+        bits, f = O.round_bf16(x)
+        return bits.reshape(x.shape), f.reshape(x.shape)
+    from paper_2506_04165_b200 import data
+    bits = data.f32_to_bf16_bits(x)
+    return bits, data.bf16_bits_to_f32(bits)
+
+
+def make_rows(cfg, r0, r1, reference=False, n=None, seed_key=None, std=1.0):
+    """Rows [r0, r1) of the config's batch: (device-dtype host array, fp32 view)."""
+    n = cfg["n"] if n is None else n
+    seed = SEEDS[seed_key or cfg["seed"]]
+    x = normal_f32(seed, r0 * n, (r1 - r0) * n, std, reference).reshape(r1 - r0, n)
     if cfg["dtype"] == "bf16":
-        bits, f = data.normal_bf16(seed, (cfg["rows"], cfg["n"]))
-        return bits, f
-    x = data.normal_f32(seed, (cfg["rows"], cfg["n"]))
+        return to_bf16(x, reference)
     return x, x
 
 
@@ -97,8 +155,9 @@ def peaks():
     if os.path.exists(path):
         with open(path) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json, copy)"
-    return 6650.0, "fallback (B200_PROFILING.md)"
+        return p, "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+        "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -174,10 +233,9 @@ def traffic_from_profiles(workload):
         return None
 
 
-
 def ref_backend():
     from oracle import pyoracle as O
-    if not O.ref_available():
+    if not O.ref_available() and os.path.isdir("/root/reference/proj/core"):
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "ref"], capture_output=True)
     if O.ref_available():
         return O.ref(), "reference"
@@ -194,43 +252,61 @@ def timed_calls(fn, steps, min_seconds, max_calls=50):
     return times
 
 
-def metric_name():
-    return "approx top-K Gelem/s & HBM GB/s vs ~8 TB/s roofline at matched expected recall"
-
-
 # ---------------------------------------------------------------------------
 # workloads
 # ---------------------------------------------------------------------------
 class RowsWorkload:
-    """C1/C2/C3: a batch of independent rows per rank (weak scaling)."""
-    scaling = "weak"
-    kernel = "stage1_flat_kernel"
+    """C1/C2/C3: a batch of independent rows.  Strong scaling: this rank owns
+    rows [r0, r1) of the BASELINE batch; the top-K of all ranks are gathered
+    every step.  Weak scaling (--weak): every rank owns a full batch."""
 
     def __init__(self, args, cfg, kp, b, rec, world, rank):
         self.args, self.cfg, self.kp, self.b, self.rec = args, cfg, kp, b, rec
         self.world, self.rank = world, rank
-        self.rows, self.n, self.k = cfg["rows"], cfg["n"], cfg["k"]
+        self.total_rows, self.n, self.k = cfg["rows"], cfg["n"], cfg["k"]
+        self.strong = not args.weak
+        if self.strong:
+            if self.total_rows % world:
+                raise SystemExit(f"{cfg['rows']} rows do not split over {world} GPUs")
+            per = self.total_rows // world
+            self.r0, self.r1 = rank * per, (rank + 1) * per
+        else:
+            self.r0, self.r1 = 0, self.total_rows
+        self.rows = self.r1 - self.r0
         self.esz = 2 if cfg["dtype"] == "bf16" else 4
         self.dtype = "bf16" if self.esz == 2 else "f32"
+        self.scaling = "strong" if self.strong else "weak"
 
     def setup(self, dev):
         import torch
         import paper_2506_04165_b200 as atk
         self.torch, self.atk, self.dev = torch, atk, dev
-        self.host, self.host_f32 = make_rows(self.cfg, self.rank)
-        if self.esz == 2:
-            self.x = torch.from_numpy(self.host.view(np.int16)).to(dev).view(torch.bfloat16)
-        else:
-            self.x = torch.from_numpy(self.host).to(dev)
-        if self.cfg["n"] != self.n:
-            raise AssertionError
+        self.host, self.host_f32 = make_rows(self.cfg, self.r0, self.r1)
+        self.x = self.to_device(self.host)
         self.p = atk.AlgoParams(self.n, self.b, self.kp, self.k)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.out = (torch.empty(self.rows, self.k, device=dev),
                     torch.empty(self.rows, self.k, dtype=torch.int32, device=dev))
+        if self.world > 1 and self.strong:
+            self.gathered = (torch.empty(self.total_rows, self.k, device=dev),
+                             torch.empty(self.total_rows, self.k, dtype=torch.int32, device=dev))
+        self.flush = None
+
+    def to_device(self, host):
+        torch = self.torch
+        if self.esz == 2:
+            return torch.from_numpy(np.ascontiguousarray(host).view(np.int16)).to(self.dev).view(torch.bfloat16)
+        return torch.from_numpy(np.ascontiguousarray(host)).to(self.dev)
+
+    def compute(self):
+        self.atk.approx_top_k_device(self.x, self.p, status=self.status, out=self.out)
 
     def step(self):
-        self.atk.approx_top_k_device(self.x, self.p, status=self.status, out=self.out)
+        self.compute()
+        if self.world > 1 and self.strong:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(self.gathered[0], self.out[0])
+            dist.all_gather_into_tensor(self.gathered[1], self.out[1])
 
     def check(self):
         self.atk.check_status(self.status)
@@ -238,33 +314,51 @@ class RowsWorkload:
     def elements(self):  # per rank per step
         return self.rows * self.n
 
+    def job_elements(self):
+        return self.total_rows * self.n if self.strong else self.rows * self.n * self.world
+
     def hbm_bytes(self):
         return self.rows * self.n * self.esz
 
     def dominant_kernel(self):
-        # the approx_top_k plan (csrc/atkg_api.cu): long rows take the threshold
-        # stream (streamthr.cuh), rows that fit in shared memory the row-resident path
-        if self.n >= 32768 and not os.environ.get("ATKG_NO_STREAMTHR"):
+        # the approx_top_k dispatch (csrc/atkg_api.cu): long rows take the
+        # threshold stream, short bf16 rows the row-resident kernels
+        if self.n >= 32768:
             return "st_stream_kernel (threshold stream; stage-1 pass)"
         if self.n * self.esz <= 64 * 1024:
             return "row_threshold_kernel" if self.kp >= 8 else "row_resident_kernel"
-        return self.kernel
+        return "stage1_flat_kernel"
 
     def roofline(self, kern_ms, ms_step):
-        peak, src = peaks()
+        pk, src = peaks()
+        peak = float(pk["hbm_gbs"])
         alg = self.rows * self.n * self.esz + self.rows * self.b * self.kp * 8
         ach = alg / (kern_ms * 1e-3) / 1e9
         return {"kernel": self.dominant_kernel(), "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
-                "peak_source": src, "unit": "GB/s", "frac": round(ach / peak, 4),
+                "peak_source": src + " copy bandwidth", "unit": "GB/s", "frac": round(ach / peak, 4),
                 "traffic": traffic_from_profiles(self.args.config), "alg_bytes_per_launch": alg,
                 "launch_ms": round(kern_ms, 5), "share_of_step": round(kern_ms / ms_step, 4)}
+
+    def result(self):
+        """(values, indices) of the whole batch on this rank (host numpy)."""
+        v, i = self.gathered if (self.world > 1 and self.strong) else self.out
+        return v.cpu().numpy(), i.cpu().numpy()
+
+    def single_gpu_result(self):
+        """The whole batch on this GPU alone (invariance check, N > 1)."""
+        torch, atk = self.torch, self.atk
+        host, _ = make_rows(self.cfg, 0, self.total_rows)
+        x = self.to_device(host)
+        v, i = atk.approx_top_k_device(x, self.p)
+        del x
+        return v.cpu().numpy(), i.cpu().numpy()
 
     def recall(self):
         atk = self.atk
         _, ei = atk.exact_top_k_device(self.x, self.k)
         rs = [atk.measure_recall(atk.TopKResult(None, self.out[1][r].cpu().numpy().astype(np.uint32)),
                                  atk.TopKResult(None, ei[r].cpu().numpy().astype(np.uint32)))
-              for r in range(self.rows)]
+              for r in range(0, self.rows, max(1, self.rows // 256))]
         return float(np.mean(rs))
 
     def e2e(self, steps, barrier):
@@ -306,7 +400,8 @@ class RowsWorkload:
             one()
         el = time.perf_counter() - t0
         assert torch.equal(oi, self.out[1].cpu()), "e2e and device results differ"
-        return el, {"h2d_bytes_per_step": rows * n * self.esz, "d2h_bytes_per_step": rows * k * 8, "api": api}
+        return el, {"h2d_bytes_per_step": rows * n * self.esz, "d2h_bytes_per_step": rows * k * 8, "api": api,
+                    "scope": "per rank (its rows), max over ranks"}
 
     def cpu_baseline(self):
         be, kind = ref_backend()
@@ -315,48 +410,54 @@ class RowsWorkload:
                                                           threads=threads), 3, 10.0)
         med = statistics.median(times)
         cores = min(threads, self.rows) if kind == "reference" else 1
+        t_ex = timed_calls(lambda: be.exact_top_k(self.host_f32[0], self.k), 1, 2.0, max_calls=5)
         return {"value": round(self.rows * self.n / med / 1e9, 4), "unit": "Gelem/s", "cores": cores, "kind": kind,
+                "cpu_model": cpu_model(),
                 "sample": f"full workload ({self.rows} rows x {self.n}) per call, median of {len(times)} calls, "
-                          f"approx_top_k_batch(threads={threads}; the reference parallelises over rows)"}
+                          f"approx_top_k_batch(threads={threads}; the reference parallelises over rows)",
+                "exact_top_k_ms_per_row": round(statistics.median(t_ex) * 1e3, 3),
+                "exact_top_k_note": "reference exact_top_k (full key sort, the recall oracle) on one row, 1 core"}
 
     def reference_sample(self):
-        """(callable, elements per call, description, cores) for --impl reference."""
+        """(callable, elements per call, description, cores, kind) for --impl reference."""
         be, kind = ref_backend()
         threads = (os.cpu_count() or 1) if kind == "reference" else 1
-        _, f = make_rows(self.cfg, 0)
+        _, f = make_rows(self.cfg, 0, min(threads, self.total_rows), reference=True)
         t0 = time.perf_counter()
-        be.approx_top_k_batch(f[:threads], self.b, self.kp, self.k, 128, threads=threads)
-        per_row = max(1e-6, (time.perf_counter() - t0) / threads)
+        be.approx_top_k_batch(f, self.b, self.kp, self.k, 128, threads=threads)
+        per_row = max(1e-6, (time.perf_counter() - t0) / f.shape[0])
         budget = min(0.1, 120.0 / max(1, self.args.steps + self.args.warmup))
-        rows = int(max(1, min(self.rows, budget / per_row)))
+        rows = int(max(1, min(self.total_rows, budget / per_row)))
+        if rows > f.shape[0]:
+            _, f = make_rows(self.cfg, 0, rows, reference=True)
         sample = np.ascontiguousarray(f[:rows])
         fn = lambda: be.approx_top_k_batch(sample, self.b, self.kp, self.k, 128, threads=threads)  # noqa: E731
-        return fn, rows * self.n, (f"{rows} of {self.rows} rows x {self.n} per step, "
+        return fn, rows * self.n, (f"{rows} of {self.total_rows} rows x {self.n} per step, "
                                    f"approx_top_k_batch(threads={threads})"), min(threads, rows), kind
 
     def config(self):
-        return {"workload": self.args.config + ": " + self.cfg["label"], "rows_per_gpu": self.rows, "n": self.n,
-                "K": self.k, "local_k": self.kp, "num_buckets": self.b, "expected_recall": round(self.rec, 6),
-                "parallelism": f"rows sharded across {self.world} GPU(s), no collective",
-                "l2": "inputs larger than L2 (no flush needed)" if self.hbm_bytes() > 126e6
-                else "L2 flushed between steps"}
+        par = (f"rows split over {self.world} GPU(s): {self.rows} per rank, top-K all-gathered (NCCL) every step"
+               if self.strong else f"every one of {self.world} GPU(s) runs its own full batch (--weak)")
+        return {"workload": self.args.config + ": " + self.cfg["label"], "rows": self.total_rows,
+                "rows_per_gpu": self.rows, "n": self.n, "K": self.k, "local_k": self.kp, "num_buckets": self.b,
+                "expected_recall": round(self.rec, 6), "parallelism": par,
+                "l2": "inputs larger than L2 (no flush needed)" if self.hbm_bytes() * self.world > 126e6
+                else "input L2-resident (parity-size config, not a bandwidth measurement)"}
 
 
 class GemmWorkload(RowsWorkload):
     """C4: fused tcgen05 GEMM with stage 1 in the epilogue, then stage 2.
-    Per rank: its own 8192 activation rows, W replicated (weak scaling)."""
-    kernel = "gemm_tc_kernel (fused stage-1 epilogue)"
+    Strong scaling: this rank's x rows, W replicated."""
 
     def setup(self, dev):
         import torch
         import paper_2506_04165_b200 as atk
-        from paper_2506_04165_b200 import data
         from paper_2506_04165_b200 import topk as T
         self.torch, self.atk, self.T, self.dev = torch, atk, T, dev
         cfg = self.cfg
         self.kdim = cfg["kdim"]
-        xb, self.x_f32 = data.normal_bf16(data.SEEDS[cfg["seed"]] + 1000 * self.rank, (self.rows, self.kdim))
-        wb, self.w_f32 = data.normal_bf16(data.SEEDS[cfg["wseed"]], (self.n, self.kdim), std=0.02)
+        xb, self.x_f32 = make_rows(cfg, self.r0, self.r1, n=self.kdim)
+        wb, self.w_f32 = make_rows(cfg, 0, self.n, n=self.kdim, seed_key=cfg["wseed"], std=0.02)
         self.host = xb
         self.x = torch.from_numpy(xb.view(np.int16)).to(dev).view(torch.bfloat16)
         self.w = torch.from_numpy(wb.view(np.int16)).to(dev).view(torch.bfloat16)
@@ -364,30 +465,39 @@ class GemmWorkload(RowsWorkload):
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.out = (torch.empty(self.rows, self.k, device=dev),
                     torch.empty(self.rows, self.k, dtype=torch.int32, device=dev))
+        if self.world > 1 and self.strong:
+            self.gathered = (torch.empty(self.total_rows, self.k, device=dev),
+                             torch.empty(self.total_rows, self.k, dtype=torch.int32, device=dev))
+        self.flush = None
 
-    def step(self):
+    def compute(self):
         self.T.fused_gemm_top_k_device(self.x, self.w, self.p, status=self.status, out=self.out)
 
-    def hbm_bytes(self):  # operands + candidates + results
+    def hbm_bytes(self):  # operands
         return (self.rows + self.n) * self.kdim * 2
 
     def flops(self):
         return 2.0 * self.rows * self.n * self.kdim
 
+    def dominant_kernel(self):
+        return "gemm_tc_kernel (tcgen05 GEMM, stage-1 epilogue)"
+
     def roofline(self, kern_ms, ms_step):
-        path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-        peak, sus, src = 1646.4, 1393.0, "measured (MEASURED_PEAKS.json, torch bf16 8192^3 burst)"
-        if os.path.exists(path):
-            with open(path) as f:
-                d = json.load(f)
-            peak, sus = float(d.get("bf16_tflops", peak)), float(d.get("bf16_tflops_sustained", sus))
-        else:
-            src = "fallback"
+        pk, src = peaks()
+        peak, sus = float(pk.get("bf16_tflops", 1590.0)), float(pk.get("bf16_tflops_sustained", 1400.0))
         ach = self.flops() / (kern_ms * 1e-3) / 1e12
-        return {"kernel": self.kernel, "bound": "tensor", "achieved": round(ach, 1), "peak": peak,
-                "peak_source": src, "peak_sustained": sus, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+        return {"kernel": self.dominant_kernel(), "bound": "tensor", "achieved": round(ach, 1), "peak": peak,
+                "peak_source": src + " cuBLAS bf16 (burst)", "peak_sustained": sus, "unit": "TFLOP/s",
+                "frac": round(ach / peak, 4), "frac_of_sustained": round(ach / sus, 4),
                 "traffic": traffic_from_profiles("C4"), "alg_flops_per_launch": self.flops(),
                 "launch_ms": round(kern_ms, 5), "share_of_step": round(kern_ms / ms_step, 4)}
+
+    def single_gpu_result(self):
+        torch = self.torch
+        xb, _ = make_rows(self.cfg, 0, self.total_rows, n=self.kdim)
+        x = torch.from_numpy(xb.view(np.int16)).to(self.dev).view(torch.bfloat16)
+        v, i = self.T.fused_gemm_top_k_device(x, self.w, self.p)
+        return v.cpu().numpy(), i.cpu().numpy()
 
     def recall(self):
         atk, T = self.atk, self.T
@@ -426,15 +536,22 @@ class GemmWorkload(RowsWorkload):
         el = time.perf_counter() - t0
         assert torch.equal(oi, self.out[1].cpu()), "e2e and device results differ"
         return el, {"h2d_bytes_per_step": self.rows * self.kdim * 2, "d2h_bytes_per_step": self.rows * self.k * 8,
-                    "api": "fused_gemm_top_k_device (pinned x H2D + D2H in the region; W resident)"}
+                    "api": "fused_gemm_top_k_device (pinned x H2D + D2H in the region; W resident)",
+                    "scope": "per rank (its rows), max over ranks"}
 
-    def _mips_sample(self, queries):
+    def _mips_sample(self, queries, reference=False):
         be, kind = ref_backend()
         threads = os.cpu_count() or 1
         if kind != "reference":
             return None
-        q = np.ascontiguousarray(self.x_f32[:queries])
-        return (lambda: be.mips_fused(self.w_f32, q, self.b, self.kp, self.k, 128, 0, threads)), threads
+        if reference:
+            _, xq = make_rows(self.cfg, 0, queries, n=self.cfg["kdim"], reference=True)
+            _, w = make_rows(self.cfg, 0, self.n, n=self.cfg["kdim"], seed_key=self.cfg["wseed"], std=0.02,
+                             reference=True)
+        else:
+            xq, w = self.x_f32[:queries], self.w_f32
+        q = np.ascontiguousarray(xq)
+        return (lambda: be.mips_fused(w, q, self.b, self.kp, self.k, 128, 0, threads)), threads
 
     def cpu_baseline(self):
         threads = os.cpu_count() or 1
@@ -446,24 +563,24 @@ class GemmWorkload(RowsWorkload):
         times = timed_calls(fn, 2, 10.0, max_calls=10)
         med = statistics.median(times)
         return {"value": round(nq * self.n / med / 1e9, 4), "unit": "Gelem/s", "cores": threads,
-                "kind": "reference",
+                "kind": "reference", "cpu_model": cpu_model(),
                 "sample": f"{nq} of {self.rows} query rows x {self.n} columns (Kd={self.kdim}) per call, reference "
                           f"mips_fused(threads={threads}) on the fp32 upcast of the same bf16 operands, median of "
                           f"{len(times)} calls"}
 
     def reference_sample(self):
         threads = os.cpu_count() or 1
-        nq = min(self.rows, 4 * threads)
-        got = self._mips_sample(nq)
+        nq = min(self.total_rows, 4 * threads)
+        got = self._mips_sample(nq, reference=True)
         if got is None:
             raise RuntimeError("reference library (oracle/_ref) not built")
         fn, threads = got
-        return fn, nq * self.n, (f"{nq} of {self.rows} query rows x {self.n} columns per step, reference "
+        return fn, nq * self.n, (f"{nq} of {self.total_rows} query rows x {self.n} columns per step, reference "
                                  f"mips_fused(threads={threads})"), threads, "reference"
 
     def config(self):
         c = super().config()
-        c.update({"kdim": self.kdim, "gemm": "x bf16 [8192, 3584] . W^T bf16 [14336, 3584], fp32 accumulate",
+        c.update({"kdim": self.cfg["kdim"], "gemm": "x bf16 [8192, 3584] . W^T bf16 [14336, 3584], fp32 accumulate",
                   "l2": "operands 161 MB > L2; scores never materialised"})
         return c
 
@@ -472,17 +589,21 @@ class GiantRowWorkload(RowsWorkload):
     """C5: one row of 2^30 fp32.  N=1: approx_top_k_device.  N>1: the row is
     sliced across ranks (shard.ShardedTopK): per-rank stage-1 summary,
     NCCL all-gather of the summaries, merge + stage 2 on every rank."""
-    scaling = "strong"
+
+    def __init__(self, args, cfg, kp, b, rec, world, rank):
+        super().__init__(args, cfg, kp, b, rec, 1, 0)
+        self.world, self.rank = world, rank
+        self.strong = True
+        self.scaling = "strong"
 
     def setup(self, dev):
         import torch
         import paper_2506_04165_b200 as atk
-        from paper_2506_04165_b200 import data
         from paper_2506_04165_b200.shard import ShardedTopK, slice_bounds
         self.torch, self.atk, self.dev = torch, atk, dev
         self.p = atk.AlgoParams(self.n, self.b, self.kp, self.k)
         self.start, self.length = slice_bounds(self.n, self.b, self.world, self.rank)
-        self.host = data.normal_f32_range(data.SEEDS[self.cfg["seed"]], self.start, self.length)
+        self.host = normal_f32(SEEDS[self.cfg["seed"]], self.start, self.length)
         self.host_f32 = self.host
         self.x = torch.from_numpy(self.host).to(dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -490,6 +611,7 @@ class GiantRowWorkload(RowsWorkload):
         # ATKG_BENCH_SHARD=1 forces the sliced path at N=1 too (NCCL group of 1)
         shard = self.world > 1 or os.environ.get("ATKG_BENCH_SHARD") == "1"
         self.sharded = ShardedTopK(self.p) if shard else None
+        self.flush = None
 
     def step(self):
         if self.sharded is None:
@@ -502,19 +624,31 @@ class GiantRowWorkload(RowsWorkload):
     def elements(self):  # per rank per step (its slice)
         return self.length
 
+    def job_elements(self):
+        return self.n
+
     def hbm_bytes(self):
         return self.length * 4
 
+    def dominant_kernel(self):
+        return ("stage1_flat_kernel (slice summaries)" if self.sharded is not None
+                else "st_stream_kernel (threshold stream; stage-1 pass)")
+
     def roofline(self, kern_ms, ms_step):
-        peak, src = peaks()
+        pk, src = peaks()
+        peak = float(pk["hbm_gbs"])
         alg = self.length * 4 + self.b * self.kp * 8
         ach = alg / (kern_ms * 1e-3) / 1e9
-        kern = ("stage1_flat_kernel (slice summaries)" if self.sharded is not None
-                else "st_stream_kernel (threshold stream; stage-1 pass)")
-        return {"kernel": kern, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
-                "peak_source": src, "unit": "GB/s", "frac": round(ach / peak, 4),
+        return {"kernel": self.dominant_kernel(), "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+                "peak_source": src + " copy bandwidth", "unit": "GB/s", "frac": round(ach / peak, 4),
                 "traffic": traffic_from_profiles("C5"), "alg_bytes_per_launch": alg,
                 "launch_ms": round(kern_ms, 5), "share_of_step": round(kern_ms / ms_step, 4)}
+
+    def result(self):
+        return self.out[0].cpu().numpy(), self.out[1].cpu().numpy()
+
+    def single_gpu_result(self):
+        return None  # the whole row lives on no single rank at N > 1 (checked by the -m gpu slice tests)
 
     def recall(self):
         if self.sharded is not None:  # the whole row lives on no single rank
@@ -552,13 +686,15 @@ class GiantRowWorkload(RowsWorkload):
         el = time.perf_counter() - t0
         assert torch.equal(oi, self.out[1][0].cpu()), "e2e and device results differ"
         return el, {"h2d_bytes_per_step": self.length * 4, "d2h_bytes_per_step": self.k * 8,
-                    "api": "approx_top_k_device / shard.ShardedTopK (pinned H2D + D2H in the region)"}
+                    "api": "approx_top_k_device / shard.ShardedTopK (pinned H2D + D2H in the region)",
+                    "scope": "per rank (its slice), max over ranks"}
 
-    def _prefix(self):
+    def _prefix(self, reference=False):
         be, kind = ref_backend()
-        m = min(self.length, 1 << 28)
+        m = min(self.length if not reference else self.n, 1 << 28)
         m -= m % self.b
-        row = np.ascontiguousarray(self.host[:m]).reshape(1, m)
+        host = normal_f32(SEEDS[self.cfg["seed"]], 0, m, reference=True) if reference else self.host[:m]
+        row = np.ascontiguousarray(host).reshape(1, m)
         return be, kind, row, m
 
     def cpu_baseline(self):
@@ -567,14 +703,15 @@ class GiantRowWorkload(RowsWorkload):
                             max_calls=5)
         med = statistics.median(times)
         return {"value": round(m / med / 1e9, 4), "unit": "Gelem/s", "cores": 1, "kind": kind,
+                "cpu_model": cpu_model(),
                 "sample": f"first {m} elements of the row as one row (same B, K', K), median of {len(times)} calls; "
                           f"the reference parallelises over rows only, so one row runs on 1 core"}
 
     def reference_sample(self):
-        be, kind, row, m = self._prefix()
-        m2 = min(m, 1 << 26)
-        r2 = np.ascontiguousarray(row[:, :m2])
-        return ((lambda: be.approx_top_k_batch(r2, self.b, self.kp, self.k, 128, threads=1)), m2,
+        be, kind = ref_backend()
+        m2 = 1 << 26
+        row = np.ascontiguousarray(normal_f32(SEEDS[self.cfg["seed"]], 0, m2, reference=True)).reshape(1, m2)
+        return ((lambda: be.approx_top_k_batch(row, self.b, self.kp, self.k, 128, threads=1)), m2,
                 f"first {m2} elements of the row as one row per step (1 core: the reference parallelises "
                 f"over rows only)", 1, kind)
 
@@ -593,26 +730,18 @@ def make_workload(args, cfg, kp, b, rec, world, rank):
     return cls(args, cfg, kp, b, rec, world, rank)
 
 
-def run_reference_arm(args, cfg, kp, b, rec):
+def run_reference_arm(args, cfg):
     """The reference's own CPU path (oracle/_ref = the unmodified atk core
     compiled from /root/reference; the C port only if that build is absent)
     with the host threads it can use, on this config's bytes.  Each step is a
     bounded sample of the workload sized so the whole --steps/--warmup run
     stays within a few minutes; the metric (elements/s) is per element, so
-    the sample size does not bias it."""
+    the sample size does not bias it.  Nothing here loads libatkg.so."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    kp, b, rec = plan(cfg, reference=True)
     wl = make_workload(args, cfg, kp, b, rec, 1, 0)
-    if cfg.get("kind") == "gemm":
-        from paper_2506_04165_b200 import data
-        wl.kdim = cfg["kdim"]
-        _, wl.x_f32 = data.normal_bf16(data.SEEDS[cfg["seed"]], (cfg["rows"], cfg["kdim"]))
-        _, wl.w_f32 = data.normal_bf16(data.SEEDS[cfg["wseed"]], (cfg["n"], cfg["kdim"]), std=0.02)
-    elif cfg.get("kind") == "giant":
-        from paper_2506_04165_b200 import data
-        wl.length = 1 << 26
-        wl.host = data.normal_f32_range(data.SEEDS[cfg["seed"]], 0, wl.length)
     fn, elems, desc, cores, kind = wl.reference_sample()
     t0 = time.perf_counter()
     fn()
@@ -627,16 +756,76 @@ def run_reference_arm(args, cfg, kp, b, rec):
         times.append(time.perf_counter() - t0)
     total = sum(times)
     val = elems * len(times) / total / 1e9
+    conf = {"workload": args.config + ": " + cfg["label"], "rows": cfg["rows"], "n": cfg["n"], "K": cfg["k"],
+            "local_k": kp, "num_buckets": b, "expected_recall": round(rec, 6)}
     line = {
         "impl": "reference", "metric": metric_name(), "value": round(val, 4), "unit": "Gelem/s",
         "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
         "ms_per_step": round(total / len(times) * 1e3, 3), "higher_is_better": True, "scaling": wl.scaling,
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded N(0,1), csrc/datagen.cpp)",
-        "config": wl.config(),
-        "cpu_baseline": {"value": round(val, 4), "unit": "Gelem/s", "cores": cores, "kind": kind, "sample": desc},
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded N(0,1), the oracle's input generator)",
+        "config": conf,
+        "cpu_baseline": {"value": round(val, 4), "unit": "Gelem/s", "cores": cores, "kind": kind, "sample": desc,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": round(val, 4), "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "product_library_loaded": "paper_2506_04165_b200" in sys.modules,
     }
     print(json.dumps(line), flush=True)
+
+
+def relaunch_under_torchrun(args):
+    """--gpus N without a torchrun environment: one process per GPU."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", os.environ.get("ATKG_BENCH_PORT", "29531"),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "WARN")
+    log("bench: relaunching under torchrun:", " ".join(cmd))
+    raise SystemExit(subprocess.call(cmd, env=env))
+
+
+def run_sweep(args):
+    """C3 K' sweep (BASELINE configs[2]): per recall target and K', the
+    planner's B, one device-timed line each (K'=1 is the original two-stage
+    algorithm).  Single GPU."""
+    import torch
+    import paper_2506_04165_b200 as atk
+    cfg = CONFIGS["C3"]
+    dev = torch.device("cuda", 0)
+    host, f = make_rows(cfg, 0, cfg["rows"])
+    x = torch.from_numpy(host.view(np.int16)).to(dev).view(torch.bfloat16)
+    _, ei = atk.exact_top_k_device(x, cfg["k"])
+    ei = ei.cpu().numpy()
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    out = (torch.empty(cfg["rows"], cfg["k"], device=dev),
+           torch.empty(cfg["rows"], cfg["k"], dtype=torch.int32, device=dev))
+    base = {}
+    for target in (0.95, 0.99):
+        for kp in (1, 2, 4, 8):
+            kp_, b, rec = plan(cfg, target=target, kps=(kp,))
+            p = atk.AlgoParams(cfg["n"], b, kp_, cfg["k"])
+            for _ in range(max(3, args.warmup)):
+                atk.approx_top_k_device(x, p, status=st, out=out)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            steps = max(10, min(args.steps, 200))
+            for _ in range(steps):
+                atk.approx_top_k_device(x, p, status=st, out=out)
+            e1.record()
+            torch.cuda.synchronize()
+            atk.check_status(st)
+            ms = e0.elapsed_time(e1) / steps
+            oi = out[1].cpu().numpy()
+            meas = float(np.mean([len(np.intersect1d(oi[r], ei[r])) / cfg["k"] for r in range(0, cfg["rows"], 8)]))
+            val = cfg["rows"] * cfg["n"] / (ms * 1e-3) / 1e9
+            if kp == 1:
+                base[target] = ms
+            print(json.dumps({"sweep": "C3 K'", "recall_target": target, "local_k": kp_, "num_buckets": b,
+                              "candidates": b * kp_, "expected_recall": round(rec, 6),
+                              "measured_recall": round(meas, 6), "ms_per_step": round(ms, 5),
+                              "value": round(val, 3), "unit": "Gelem/s",
+                              "speedup_vs_kprime1": round(base[target] / ms, 3) if target in base else None}),
+                  flush=True)
 
 
 def main():
@@ -646,16 +835,23 @@ def main():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=list(CONFIGS))
+    ap.add_argument("--weak", action="store_true", help="every rank runs its own full batch")
+    ap.add_argument("--sweep", action="store_true", help="C3 K' sweep lines (single GPU)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-recall", action="store_true", help="skip the measured-recall check")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
-    kp, b, rec = plan(cfg)
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
 
     if args.impl == "reference":
-        run_reference_arm(args, cfg, kp, b, rec)
+        run_reference_arm(args, cfg)
+        return
+    if args.sweep:
+        run_sweep(args)
         return
 
     import torch
@@ -664,6 +860,7 @@ def main():
     import paper_2506_04165_b200 as atk
     from paper_2506_04165_b200._lib import lib
 
+    kp, b, rec = plan(cfg)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -671,9 +868,12 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1 or (cfg.get("kind") == "giant" and os.environ.get("ATKG_BENCH_SHARD") == "1"):
         dist.init_process_group("nccl", device_id=dev)
+        world = dist.get_world_size()
+    if args.gpus != world:
+        log(f"bench: --gpus {args.gpus} but the process group has {world} rank(s); reporting {world}")
 
     def barrier():
-        if world > 1:
+        if dist.is_initialized() and world > 1:
             dist.barrier()
 
     wl = make_workload(args, cfg, kp, b, rec, world, rank)
@@ -690,6 +890,7 @@ def main():
     launches0 = lib.atkg_launch_count()
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
+        barrier()
         # dominant-kernel CUDA events on every 16th step only: a bracket sits
         # between that kernel and its PDL-launched successor
         lib.atkg_profile_begin_every(int(os.environ.get("ATKG_BENCH_PROF_EVERY", "16")))
@@ -712,11 +913,21 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, kern_ms = float(t[0]), float(t[1])
     ms_step = ms / args.steps
-    elems = wl.elements() * (world if wl.scaling == "weak" else 1)
-    if wl.scaling == "strong":
-        elems = cfg["rows"] * cfg["n"]
-    value = elems / (ms_step * 1e-3) / 1e9  # Gelem/s, whole job
+    # a bracket holds exactly one launch of the dominant kernel; for one-kernel
+    # steps it cannot exceed the step (the bracket would include launch gaps)
+    kern_ms = min(kern_ms, ms_step) if kern_ms > 0 else ms_step
+    value = wl.job_elements() / (ms_step * 1e-3) / 1e9  # Gelem/s, whole job
     hbm_gbs = wl.hbm_bytes() * world / (ms_step * 1e-3) / 1e9
+
+    invariance = None
+    if world > 1:
+        if rank == 0:
+            ref = wl.single_gpu_result()
+            if ref is not None:
+                got = wl.result()
+                invariance = bool(np.array_equal(np.asarray(got[0]).view(np.uint32), ref[0].view(np.uint32))
+                                  and np.array_equal(np.asarray(got[1]), ref[1]))
+        barrier()
 
     recall = None if args.no_recall else wl.recall()
     roof = wl.roofline(kern_ms, ms_step)
@@ -727,7 +938,7 @@ def main():
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     el = float(te[0])
-    e2e = {"value": round(elems * e2e_steps / el / 1e9, 4), "unit": "Gelem/s",
+    e2e = {"value": round(wl.job_elements() * e2e_steps / el / 1e9, 4), "unit": "Gelem/s",
            "ms_per_step": round(el / e2e_steps * 1e3, 3), **e2e_info}
 
     cpu = None
@@ -737,14 +948,17 @@ def main():
     if rank == 0:
         line = {"metric": metric_name(), "value": round(value, 3), "unit": "Gelem/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-                "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": wl.dtype,
+                "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None,
+                "dtype": "bf16" if cfg["dtype"] == "bf16" else "f32",
                 "data": "synthetic (seeded N(0,1), csrc/datagen.cpp)", "config": wl.config(),
                 "hbm_gbs": round(hbm_gbs, 1),
                 "recall": {"expected": round(rec, 6), "measured": None if recall is None else round(recall, 6)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
                 "gpu_launches": int(launches)}
+        if invariance is not None:
+            line["split_invariance"] = invariance
         if cfg.get("kind") == "gemm":
-            line["tflops"] = round(wl.flops() * (world if wl.scaling == "weak" else 1) / (ms_step * 1e-3) / 1e12, 1)
+            line["tflops"] = round(wl.flops() * world / (ms_step * 1e-3) / 1e12, 1)
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.barrier()

@@ -87,6 +87,41 @@ void orc_uniform_below(uint64_t seed, uint64_t bound, uint64_t count, float* out
   for (uint64_t i = 0; i < count; ++i) out[i] = (float)xo_below(&x, bound);
 }
 
+/* ---- seeded normal inputs (the build's input convention) ---
+ * A second, independent statement of csrc/datagen.cpp, so the reference arm
+ * of bench.py can make its inputs without the product library: block q of
+ * 65536 elements draws Box-Muller pairs from xoshiro256++(derive_seed(seed,
+ * q)); z = sqrt(-2 ln(1-u1)) (cos, sin)(2 pi u2) in double, rounded once to
+ * fp32.  tests/test_oracle.py pins the two byte for byte. */
+void orc_fill_normal_range(uint64_t seed, uint64_t start, uint64_t count, float mean, float stddev,
+                           float* out) {
+  const uint64_t blk = 65536, q0 = start / blk;
+  const double two_pi = 6.283185307179586476925286766559;
+  for (uint64_t qq = 0; qq * blk < count; ++qq) {
+    xoshiro x; xo_init(&x, orc_derive_seed(seed, q0 + qq));
+    const uint64_t i0 = qq * blk, i1 = count < i0 + blk ? count : i0 + blk;
+    for (uint64_t i = i0; i < i1; i += 2) {
+      const double u1 = xo_double(&x), u2 = xo_double(&x);
+      const double r = sqrt(-2.0 * log(1.0 - u1)), a = two_pi * u2;
+      out[i] = (float)((double)mean + (double)stddev * (r * cos(a)));
+      if (i + 1 < i1) out[i + 1] = (float)((double)mean + (double)stddev * (r * sin(a)));
+    }
+  }
+}
+/* round-to-nearest-even fp32 -> bf16 -> fp32 (the bf16 configs' exact values) */
+void orc_round_bf16(const float* in, uint64_t count, float* out, uint16_t* bits) {
+  for (uint64_t i = 0; i < count; ++i) {
+    uint32_t u;
+    memcpy(&u, &in[i], 4);
+    uint16_t h;
+    if ((u & 0x7fffffffu) > 0x7f800000u) h = (uint16_t)((u >> 16) | 0x40u);
+    else h = (uint16_t)((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+    if (bits) bits[i] = h;
+    const uint32_t v = (uint32_t)h << 16;
+    memcpy(&out[i], &v, 4);
+  }
+}
+
 /* ---- params validation: src/topk.cpp:54-67 ------------------------------ */
 int orc_validate(uint64_t n, uint64_t b, uint32_t kp, uint32_t k, uint32_t lane) {
   if (n == 0) return fail("n must be >= 1");

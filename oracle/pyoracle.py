@@ -90,6 +90,8 @@ class _Backend:
             lib.orc_shuffled_iota.argtypes = [_u64, _u64, _f32p]
             lib.orc_uniform_below.argtypes = [_u64, _u64, _u64, _f32p]
             lib.orc_xoshiro_fill.argtypes = [_u64, _u64, _u64p]
+            lib.orc_fill_normal_range.argtypes = [_u64, _u64, _u64, C.c_float, C.c_float, _f32p]
+            lib.orc_round_bf16.argtypes = [_f32p, _u64, _f32p, C.c_void_p]
             lib.orc_derive_seed.argtypes = [_u64, _u64]
             lib.orc_derive_seed.restype = _u64
             lib.orc_score_block.argtypes = [_f32p, _u64, _f32p, _u64, _u64, _u64, _f32p, _u64]
@@ -280,3 +282,23 @@ def uniform_below(seed: int, bound: int, count: int) -> np.ndarray:
 
 def derive_seed(seed: int, stream: int) -> int:
     return int(port().lib.orc_derive_seed(seed, stream))
+
+
+def normal_f32(seed: int, start: int, count: int, mean: float = 0.0, std: float = 1.0) -> np.ndarray:
+    """The build's seeded N(mean, std) stream, elements [start, start + count)
+    (start % 65536 == 0), computed by the oracle port -- for callers that must
+    not load the product library (bench.py --impl reference)."""
+    if start % 65536:
+        raise ValueError("start must be a multiple of 65536")
+    out = np.empty(count, np.float32)
+    port().lib.orc_fill_normal_range(seed, start, count, mean, std, out)
+    return out
+
+
+def round_bf16(x: np.ndarray):
+    """(bf16 bits, exact fp32 values) of fp32 x, round to nearest even."""
+    x = np.ascontiguousarray(x, np.float32).reshape(-1)
+    out = np.empty_like(x)
+    bits = np.empty(x.size, np.uint16)
+    port().lib.orc_round_bf16(x, x.size, out, bits.ctypes.data)
+    return bits, out

@@ -227,3 +227,20 @@ def test_port_matches_ref_random(port, ref):
         a = port.approx_top_k(row, B, kp, k, lane=1)
         b = ref.approx_top_k(row, B, kp, k, lane=1)
         assert np.array_equal(bits(a[0]), bits(b[0])) and np.array_equal(a[1], b[1])
+
+
+def test_oracle_generator_matches_product_generator():
+    """The oracle's statement of the input convention (used by the reference
+    arm of bench.py, which must not load libatkg.so) is byte-identical to
+    csrc/datagen.cpp, including ragged tails and bf16 rounding."""
+    from oracle import pyoracle as O
+    from paper_2506_04165_b200 import data
+    for seed, start, count in [(2, 0, 3 * 65536 + 5), (3, 65536 * 7, 131071), (6, 0, 1)]:
+        a = O.normal_f32(seed, start, count)
+        b = data.normal_f32_range(seed, start, count)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    x = data.normal_f32(4, (100000,), std=0.02)
+    bits, f = O.round_bf16(x)
+    pb = data.f32_to_bf16_bits(x)
+    assert np.array_equal(bits, pb)
+    assert np.array_equal(f.view(np.uint32), data.bf16_bits_to_f32(pb).view(np.uint32))
