@@ -26,6 +26,9 @@ INPUTS = {
     "c3_k2": dict(kind="normal_bf16", seed=3, rows=48, n=14336, B=512, kp=2, k=287),
     "c3_k8": dict(kind="normal_bf16", seed=3, rows=48, n=14336, B=128, kp=8, k=287),
     "c3_r99": dict(kind="normal_bf16", seed=3, rows=48, n=14336, B=256, kp=4, k=287),
+    # the rest of the C3 r = 0.99 sweep (planner: K'=1 -> B=7168, K'=2 -> B=1024)
+    "c3_r99_k1": dict(kind="normal_bf16", seed=3, rows=48, n=14336, B=7168, kp=1, k=287),
+    "c3_r99_k2": dict(kind="normal_bf16", seed=3, rows=48, n=14336, B=1024, kp=2, k=287),
     # giant-row split path at reduced size (many segments per bucket)
     "c5_mini": dict(kind="normal", seed=6, rows=1, n=1 << 22, B=256, kp=8, k=1024),
     # test_topk.cpp:177-188 (simulation scale vs per-bucket sort)

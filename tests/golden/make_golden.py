@@ -70,7 +70,8 @@ def main():
         (262144, 1024, 0.95, (1, 2, 3, 4), 1), (262144, 1024, 0.95, (1,), 1), (262144, 1024, 0.99, (1, 2, 3, 4), 1),
         (430080, 3360, 0.9, (1, 2, 3, 4), 1), (262144, 64, 0.95, (1, 2, 4), 0), (14336, 287, 0.95, (1, 2, 4, 8), 0),
         (14336, 287, 0.99, (1, 2, 4, 8), 0), (14336, 287, 0.95, (1,), 0), (14336, 287, 0.95, (2,), 0),
-        (14336, 287, 0.95, (8,), 0), (14336, 287, 0.99, (1,), 0), (2**30, 1024, 0.95, (8,), 0),
+        (14336, 287, 0.95, (8,), 0), (14336, 287, 0.99, (1,), 0), (14336, 287, 0.99, (2,), 0),
+        (14336, 287, 0.99, (4,), 0), (14336, 287, 0.99, (8,), 0), (2**30, 1024, 0.95, (8,), 0),
         (32768, 128, 0.95, (1, 2, 3, 4), 0),
     ]:
         p = ref.select_parameters(n, k, t, kps, 128, seed)
