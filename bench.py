@@ -631,8 +631,8 @@ class GiantRowWorkload(RowsWorkload):
         return self.length * 4
 
     def dominant_kernel(self):
-        return ("stage1_flat_kernel (slice summaries)" if self.sharded is not None
-                else "st_stream_kernel (threshold stream; stage-1 pass)")
+        return ("st_stream_kernel (threshold stream over this rank's slice; payload exchange)"
+                if self.sharded is not None else "st_stream_kernel (threshold stream; stage-1 pass)")
 
     def roofline(self, kern_ms, ms_step):
         pk, src = peaks()
@@ -717,9 +717,15 @@ class GiantRowWorkload(RowsWorkload):
 
     def config(self):
         c = super().config()
-        c["parallelism"] = (f"one row sliced across {self.world} GPUs ({self.length} elements each), NCCL "
-                            f"all-gather of the {(2 * self.kp + 2) * self.b * 4} B stage-1 summaries"
-                            if self.world > 1 else "1 GPU")
+        if self.sharded is not None:
+            from paper_2506_04165_b200 import slice_payload_words
+            pw = slice_payload_words(self.p, self.world) * 4
+            c["parallelism"] = (f"one row sliced across {self.world} GPU(s) ({self.length} elements each): "
+                                f"threshold-stream payloads ({pw} B per rank) all-gathered over NCCL, merged on "
+                                f"every rank; exact-summary fallback when the gate is set "
+                                f"(fallbacks this run: {self.sharded.fallbacks})")
+        else:
+            c["parallelism"] = "1 GPU"
         c["rows_per_gpu"] = 1
         return c
 
@@ -867,6 +873,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 or (cfg.get("kind") == "giant" and os.environ.get("ATKG_BENCH_SHARD") == "1"):
+        for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533"), ("RANK", "0"), ("WORLD_SIZE", "1")):
+            os.environ.setdefault(k, v)
         dist.init_process_group("nccl", device_id=dev)
         world = dist.get_world_size()
     if args.gpus != world:

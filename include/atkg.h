@@ -159,6 +159,44 @@ int atkg_summary_merge_top_k(const uint32_t* d_summaries, uint32_t parts, const 
                              uint32_t* d_out_idx, void* d_ws, size_t ws_bytes,
                              uint32_t* d_status, void* stream);
 
+/* ---- one row sliced across GPUs: threshold-stream payloads --------------
+ * The fast form of the slice exchange (the same reference contract as the
+ * summaries above).  Each rank reduces its slice to a payload of
+ * atkg_slice_payload_words(p, parts) uint32 words -- every element of the
+ * slice >= the slice's threshold, global positions -- a few KB instead of
+ * the exact summaries, at the streaming speed of the threshold stream.
+ * atkg_payload_merge_top_k over the `parts` payloads (index order) writes the
+ * top global_k, or sets *d_gate (device word) when the payloads cannot
+ * settle the row (overflow, NaN, too few candidates); every rank sees the
+ * same payloads, so all of them then take the exact summary path together. */
+int atkg_slice_payload_words(const atkg_params* p, uint32_t parts, size_t* words);
+int atkg_slice_payload_workspace(int dtype, uint64_t len, const atkg_params* p, uint32_t parts,
+                                 size_t* bytes);
+int atkg_slice_payload(int dtype, const void* d_slice, uint64_t len, uint64_t index_offset,
+                       const atkg_params* p, uint32_t parts, uint32_t* d_payload, void* d_ws,
+                       size_t ws_bytes, uint32_t* d_status, void* stream);
+int atkg_payload_merge_top_k(const uint32_t* d_payloads, uint32_t parts, const atkg_params* p,
+                             float* d_out_vals, uint32_t* d_out_idx, uint32_t* d_gate,
+                             uint32_t* d_status, void* stream);
+
+/* The whole sharded approx_top_k of one row over an NCCL communicator
+ * (ncclComm_t passed as void*; rank r of `world` holds elements
+ * [index_offset, index_offset + len)): slice payload -> ncclAllGather ->
+ * merge; when the gate is set, exact summaries -> ncclAllGather -> merge.
+ * Every rank returns the same top global_k, bit-identical to approx_top_k on
+ * the whole row (topk.cpp:238-258).  Synchronises `stream` once (the gate).
+ * NCCL is loaded at run time (libnccl.so.2, the process's own if loaded);
+ * the helpers below create communicators with that same library. */
+int atkg_sharded_workspace_size(int dtype, uint64_t len, const atkg_params* p, uint32_t world,
+                                size_t* bytes);
+int atkg_sharded_approx_top_k(int dtype, const void* d_slice, uint64_t len, uint64_t index_offset,
+                              const atkg_params* p, void* nccl_comm, uint32_t world,
+                              float* d_out_vals, uint32_t* d_out_idx, void* d_ws, size_t ws_bytes,
+                              uint32_t* d_status, void* stream);
+int atkg_nccl_unique_id(char out[128]);
+int atkg_nccl_comm_init(void** comm, int nranks, const char id[128], int rank);
+int atkg_nccl_comm_destroy(void* comm);
+
 /* Synchronises `stream`, reads *d_status and maps the flags to a status
  * code (ATKG_ENAN / ATKG_EINVAL with the reference message). */
 int atkg_check_status(const uint32_t* d_status, void* stream);

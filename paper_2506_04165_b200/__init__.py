@@ -19,6 +19,7 @@ from .topk import (AlgoParams, Stage1Accumulator, TopKResult, approx_top_k, appr
                    approx_top_k_device, exact_top_k, exact_top_k_device, kDefaultLaneMultiple, kNegInf,
                    measure_recall, partition_index, select_candidates_device, select_top_k_candidates,
                    stage1_device, stage1_partial_reduce, stage1_summary_device, summary_merge_top_k_device,
-                   summary_words)
+                   summary_words, slice_payload_words, slice_payload_device, payload_merge_top_k_device,
+                   NcclComm, sharded_approx_top_k_device)
 
 __version__ = "0.1.0"

@@ -69,6 +69,15 @@ def _load():
         "atkg_stage1_summary": ([i32, vp, u64, u64, P, vp, vp, C.c_size_t, vp, vp], i32),
         "atkg_summary_merge_top_k": ([vp, u32, P, vp, vp, vp, vp, vp, C.c_size_t, vp, vp], i32),
         "atkg_check_status": ([vp, vp], i32),
+        "atkg_slice_payload_words": ([P, u32, sz], i32),
+        "atkg_slice_payload_workspace": ([i32, u64, P, u32, sz], i32),
+        "atkg_slice_payload": ([i32, vp, u64, u64, P, u32, vp, vp, C.c_size_t, vp, vp], i32),
+        "atkg_payload_merge_top_k": ([vp, u32, P, vp, vp, vp, vp, vp], i32),
+        "atkg_sharded_workspace_size": ([i32, u64, P, u32, sz], i32),
+        "atkg_sharded_approx_top_k": ([i32, vp, u64, u64, P, vp, u32, vp, vp, vp, C.c_size_t, vp, vp], i32),
+        "atkg_nccl_unique_id": ([C.c_char_p], i32),
+        "atkg_nccl_comm_init": ([C.POINTER(vp), i32, C.c_char_p, i32], i32),
+        "atkg_nccl_comm_destroy": ([vp], i32),
         "atkg_accumulator_create": ([P, C.POINTER(vp)], i32),
         "atkg_accumulator_consume": ([vp, i32, vp, u64, vp], i32),
         "atkg_accumulator_consumed": ([vp], u64),

@@ -19,6 +19,19 @@ struct Unsupported : std::runtime_error { using std::runtime_error::runtime_erro
 
 void set_last_error(const std::string& m);
 
+// re-raises a status code returned by another entry point (inside guarded())
+inline void rethrow(int rc) {
+  if (rc == ATKG_OK) return;
+  const std::string m = atkg_last_error();
+  switch (rc) {
+    case ATKG_ENAN: throw NanInput();
+    case ATKG_EINFEASIBLE: throw Infeasible(m);
+    case ATKG_ECUDA: throw CudaError(m);
+    case ATKG_EUNSUPPORTED: throw Unsupported(m);
+    default: throw Inval(m);
+  }
+}
+
 template <class F>
 int guarded(F&& f) {
   try {

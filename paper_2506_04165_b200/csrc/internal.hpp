@@ -126,7 +126,15 @@ struct StPlan {
 };
 // for_size: ignore the ATKG_NO_STREAMTHR switch (workspace sizing covers every path)
 StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
-                      bool for_size = false);
+                      bool for_size = false, double t_scale = 1.0);
+double streamthr_target(uint64_t n, uint64_t B, uint32_t kp, uint32_t k);
+void run_stream_only(int dtype, const StPlan& sp, const void* in, uint64_t n, void* ws, uint32_t* status,
+                     cudaStream_t st);
+void run_slice_payload(const StPlan& sp, const uint32_t* slots, uint32_t cap, uint64_t index_offset,
+                       const uint32_t* status, uint32_t* payload, cudaStream_t st);
+void run_payload_finish(const uint32_t* payloads, uint32_t parts, uint32_t slot_cap, uint64_t n, uint64_t B,
+                        uint32_t kp, uint32_t k, float* ov, uint32_t* oi, uint32_t* gate, uint32_t* status,
+                        cudaStream_t st);
 void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
                    uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
 

@@ -62,8 +62,22 @@ void launch_finish(const StPlan& sp, uint64_t rows, const StFinArgs& a, cudaStre
 
 }  // namespace
 
+// target count T of row elements >= L: B * E[min(K', Poisson(T/B))] must
+// clear K with margin
+double streamthr_target(uint64_t n, uint64_t B, uint32_t kp, uint32_t k) {
+  const double need = 1.2 * k + 4.0 * std::sqrt((double)k) + 8.0;
+  thread_local uint64_t t_n = 0, t_B = 0, t_kp = 0, t_k = 0;
+  thread_local double t_T = 1.0;
+  if (t_n != n || t_B != B || t_kp != kp || t_k != k) {
+    double T0 = 1.0;
+    while (T0 < (double)n && (double)B * mean_min_poisson(T0 / (double)B, kp) < need) T0 *= 1.05;
+    t_n = n; t_B = B; t_kp = kp; t_k = k; t_T = T0;
+  }
+  return t_T;
+}
+
 StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
-                      bool for_size) {
+                      bool for_size, double t_scale) {
   StPlan sp;
   if (!for_size && opt("no_streamthr", 0)) return sp;
   if (kp != 1 && kp != 2 && kp != 4 && kp != 8) return sp;
@@ -108,17 +122,9 @@ StPlan plan_streamthr(int dtype, const void* in, uint64_t rows, uint64_t n, uint
     m_vtot = sp.vtot; m_psz = sp.psz; m_nvrow = nvrow; m_smax = smax;
   }
   sp.smax = (uint32_t)m_smax;
-  // target count T of row elements >= L: B * E[min(K', Poisson(T/B))] must
-  // clear K with margin; every warp sub-stream keeps ~2x its share of T
-  const double need = 1.2 * k + 4.0 * std::sqrt((double)k) + 8.0;
-  thread_local uint64_t t_n = 0, t_B = 0, t_kp = 0, t_k = 0;
-  thread_local double t_T = 1.0;
-  if (t_n != n || t_B != B || t_kp != kp || t_k != k) {
-    double T0 = 1.0;
-    while (T0 < (double)n && (double)B * mean_min_poisson(T0 / (double)B, kp) < need) T0 *= 1.05;
-    t_n = n; t_B = B; t_kp = kp; t_k = k; t_T = T0;
-  }
-  const double T = t_T;
+  // every warp sub-stream keeps ~2x its share of the target T (a slice of a
+  // sharded row: t_scale = its share of the row's target)
+  const double T = std::max(8.0, streamthr_target(n, B, kp, k) * t_scale);
   sp.rfac = (float)(2.0 * T / (double)n);
   sp.lfac = (float)(T / 1.5 / (double)n);
   // rows cut into many pieces (the giant row): cap each slot at ~3x its share
@@ -167,6 +173,7 @@ void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, u
   f.smax = sp.smax;
   f.B = (uint32_t)B;
   f.k = k;
+  f.slot_cap = kStSlotCap;
   f.ecap = sp.ecap;
   f.slots = static_cast<const uint32_t*>(ws);
   f.out_v = ov;
@@ -196,6 +203,85 @@ void run_streamthr(int dtype, const StPlan& sp, const void* in, uint64_t rows, u
     ATKG_ST_FIN(float)
   }
 #undef ATKG_ST_FIN
+}
+
+// the stream kernel alone (no finish): slots of rows x n into ws
+void run_stream_only(int dtype, const StPlan& sp, const void* in, uint64_t n, void* ws, uint32_t* status,
+                     cudaStream_t st) {
+  StArgs a;
+  a.in = in;
+  a.n = n;
+  a.vtot = sp.vtot;
+  a.psz = sp.psz;
+  a.G = sp.G;
+  a.smax = sp.smax;
+  a.slot_bytes = sp.slot_bytes;
+  a.ns = sp.ns;
+  a.rfac = sp.rfac;
+  a.lfac = sp.lfac;
+  a.cfac = sp.cfac;
+  a.warp_sample = (uint32_t)opt("st_warp_sample", 0);
+  a.slots = static_cast<uint32_t*>(ws);
+  a.gate = nullptr;
+  a.status = status;
+  g_prof.bracket_begin(st);
+  if (dtype == ATKG_BF16) {
+    if (sp.slot_bytes == (uint32_t)kStNW * 4096) launch_stream<__nv_bfloat16, 8>(sp, a, st);
+    else launch_stream<__nv_bfloat16, 4>(sp, a, st);
+  } else {
+    if (sp.slot_bytes == (uint32_t)kStNW * 4096) launch_stream<float, 8>(sp, a, st);
+    else launch_stream<float, 4>(sp, a, st);
+  }
+  g_prof.bracket_end(st);
+}
+
+// st_finish_kernel over `parts` slice payloads (slots of slot_cap entries) as
+// the slots of one row of n elements; gate mode (no input to fall back on)
+void run_payload_finish(const uint32_t* payloads, uint32_t parts, uint32_t slot_cap, uint64_t n, uint64_t B,
+                        uint32_t kp, uint32_t k, float* ov, uint32_t* oi, uint32_t* gate, uint32_t* status,
+                        cudaStream_t st) {
+  StPlan sp;
+  sp.ecap = 8192;
+  while (sp.ecap < B * std::min<uint64_t>(kp, n / B)) sp.ecap <<= 1;
+  sp.smem_fin = (size_t)sp.ecap * 16 + (size_t)B * 12;
+  StFinArgs f{};
+  f.in = nullptr;
+  f.n = n;
+  const uint64_t nvrow = n / 4;  // the geometry only locates the slots: one row over `parts` pieces
+  f.vtot = nvrow;
+  f.psz = (nvrow + parts - 1) / parts;
+  f.G = parts;
+  f.smax = 1;
+  f.B = (uint32_t)B;
+  f.k = k;
+  f.slot_cap = slot_cap;
+  f.ecap = sp.ecap;
+  f.force_slow = (uint32_t)opt("st_force_slow", 0);
+  f.gate = gate;
+  f.slots = payloads;
+  f.out_v = ov;
+  f.out_i = oi;
+  f.status = status;
+  switch (kp) {
+    case 1: launch_finish<float, 1>(sp, 1, f, st); break;
+    case 2: launch_finish<float, 2>(sp, 1, f, st); break;
+    case 4: launch_finish<float, 4>(sp, 1, f, st); break;
+    default: launch_finish<float, 8>(sp, 1, f, st); break;
+  }
+}
+
+void run_slice_payload(const StPlan& sp, const uint32_t* slots, uint32_t cap, uint64_t index_offset,
+                       const uint32_t* status, uint32_t* payload, cudaStream_t st) {
+  StPayArgs a;
+  a.slots = slots;
+  a.G = sp.G;
+  a.smax = sp.smax;
+  a.cap = cap;
+  a.index_offset = index_offset;
+  a.status = status;
+  a.payload = payload;
+  st_slice_payload_kernel<<<1, 1024, 0, st>>>(a);
+  check_launch();
 }
 
 bool run_select_ranked(const float* vals, const uint32_t* idx, uint64_t rows, uint64_t count, uint64_t stride,

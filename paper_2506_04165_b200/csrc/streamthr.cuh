@@ -42,6 +42,7 @@
 #include "ptx.cuh"
 #include "rowthr.cuh"
 #include "summ.cuh"
+#include "stconst.hpp"
 
 namespace atkg {
 
@@ -57,10 +58,6 @@ constexpr int kStNW = ATKG_ST_NW;           // consumer warps per CTA
 #endif
 constexpr uint32_t kStLog = ATKG_ST_LOG;   // log entries per warp
 constexpr uint32_t kStWarpCap = 128;  // entries a warp keeps at a flush
-constexpr uint32_t kStSlotCap = 1024;  // entries per (piece, row segment) slot
-constexpr uint32_t kStSlotWords = 2 + 2 * kStSlotCap;  // {count, Lkey} | keys | positions
-constexpr uint32_t kStBadCount = 0xffffffffu;
-constexpr uint32_t kStMaxRowPieces = 2048;  // pieces one row may span (host-checked)
 constexpr uint32_t kStFewSlots = 3;         // finish: one-round-trip gather up to this many slots
 
 struct StArgs {
@@ -619,6 +616,7 @@ struct StFinArgs {
   const void* in;
   uint64_t n, vtot, psz;
   uint32_t G, smax, B, k;
+  uint32_t slot_cap;    // entries per slot (kStSlotCap for the stream's own slots)
   uint32_t ecap;   // gathered-entry capacity (shared memory)
   uint32_t force_slow;  // tests: every row takes the exact fallback
   uint32_t* gate;       // giant rows: no in-kernel fallback, flag the row for the host instead
@@ -662,7 +660,7 @@ __global__ void __launch_bounds__(1024) st_finish_kernel(StFinArgs a) {
   const uint32_t seg_a = (uint32_t)(row - (uint64_t)ca * a.psz / nvrow);
   const uint32_t nslots = cb - ca + 1;
   auto slot_ptr = [&](uint32_t q) {
-    return a.slots + ((uint64_t)(ca + q) * a.smax + (q == 0 ? seg_a : 0u)) * kStSlotWords;
+    return a.slots + ((uint64_t)(ca + q) * a.smax + (q == 0 ? seg_a : 0u)) * (2ull + 2ull * a.slot_cap);
   };
   __syncthreads();  // counters initialised
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the stream kernel's slots are complete
@@ -671,7 +669,7 @@ __global__ void __launch_bounds__(1024) st_finish_kernel(StFinArgs a) {
   // some slot), entry counts -> prefix pfx[]
   const int lane = t & 31;
   uint32_t Lk;
-  if (nslots <= kStFewSlots && a.ecap >= 1024 && nt >= 256 && kStSlotCap % nt == 0) {
+  if (nslots <= kStFewSlots && a.ecap >= 1024 && nt >= 256 && kStSlotCap % nt == 0 && a.slot_cap == kStSlotCap) {
     // few slots (rows over a handful of pieces): every thread reads the
     // headers (broadcast) and, speculatively, its share of every slot's
     // entries in the same round trip; filter against L = max threshold
@@ -721,7 +719,7 @@ __global__ void __launch_bounds__(1024) st_finish_kernel(StFinArgs a) {
     if (t < 32) {
       const uint32_t* sl = lane < (int)nslots ? slot_ptr(lane) : nullptr;
       const uint32_t m0 = sl ? sl[0] : 0u, l0 = sl ? sl[1] : 0u;
-      const bool bad = m0 > kStSlotCap;
+      const bool bad = m0 > a.slot_cap;
       const uint32_t m = bad ? 0u : m0;
       uint32_t incl = m;
 #pragma unroll
@@ -744,9 +742,9 @@ __global__ void __launch_bounds__(1024) st_finish_kernel(StFinArgs a) {
       const uint32_t* sl = slot_ptr(q);
       const uint32_t m = sl[0];
       lmax = max(lmax, sl[1]);
-      if (m > kStSlotCap) sh_bad = 1u;
-      pfx[q] = m > kStSlotCap ? 0u : m;
-      sum += m > kStSlotCap ? 0u : m;
+      if (m > a.slot_cap) sh_bad = 1u;
+      pfx[q] = m > a.slot_cap ? 0u : m;
+      sum += m > a.slot_cap ? 0u : m;
     }
     lmax = __reduce_max_sync(0xffffffffu, lmax);
     if (lane == 0 && lmax) atomicMax(&sh_l, lmax);
@@ -787,7 +785,7 @@ __global__ void __launch_bounds__(1024) st_finish_kernel(StFinArgs a) {
       if (e < E && key[u] >= Lk) {
         const uint32_t d = atomicAdd(&sh_ne, 1u);
         if (d < a.ecap) {
-          const uint32_t pos = slot_ptr(q[u])[2 + kStSlotCap + (e - pfx[q[u]])];
+          const uint32_t pos = slot_ptr(q[u])[2 + a.slot_cap + (e - pfx[q[u]])];
           ek[d] = key[u];
           ep[d] = pos;
           atomicAdd(&cnt[bucket(pos)], 1u);
@@ -896,6 +894,74 @@ __global__ void __launch_bounds__(1024) st_finish_kernel(StFinArgs a) {
     const uint64_t key = cand[q];
     a.out_v[row * a.k + q] = __uint_as_float(key_value_bits(key));
     a.out_i[row * a.k + q] = (uint32_t)key;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Slices of one row on different GPUs (the sharded giant row).
+// A slice runs the threshold stream as a row of its own; this kernel then
+// folds the slice's stream slots into ONE payload slot {count, Lkey,
+// keys[cap], positions[cap]} holding every element of the slice >= Lkey (Lkey
+// = the max of the slots' thresholds), positions made global by
+// index_offset.  The payloads of all slices are exchanged (all-gather) and
+// st_finish_kernel runs on them as the slots of one row: L = the max of the
+// slice thresholds, exact for the same reason as within one GPU.  A payload
+// with count kStBadCount (a slot overflowed, the slice held a NaN, or more
+// than cap entries) sends every rank to the exact summary path.
+// ---------------------------------------------------------------------------
+struct StPayArgs {
+  const uint32_t* slots;  // the slice's stream slots [G][smax][kStSlotWords]; the slice is segment 0
+  uint32_t G, smax, cap;
+  uint64_t index_offset;
+  const uint32_t* status;  // the stream kernel's flags (NaN)
+  uint32_t* payload;       // [2 + 2 cap]
+};
+
+__global__ void __launch_bounds__(1024) st_slice_payload_kernel(StPayArgs a) {
+  __shared__ uint32_t sh_l, sh_bad, sh_n;
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
+  if (t == 0) { sh_l = 0; sh_bad = (*a.status & ATKG_FLAG_NAN) ? 1u : 0u; sh_n = 0; }
+  __syncthreads();
+  auto slot = [&](uint32_t q) { return a.slots + (uint64_t)q * a.smax * kStSlotWords; };
+  uint32_t lmax = 0, bad = 0;
+  for (uint32_t q = t; q < a.G; q += nt) {
+    const uint32_t* sl = slot(q);
+    bad |= sl[0] > kStSlotCap ? 1u : 0u;
+    lmax = max(lmax, sl[1]);
+  }
+  lmax = __reduce_max_sync(0xffffffffu, lmax);
+  if ((t & 31) == 0) atomicMax(&sh_l, lmax);
+  if (bad) sh_bad = 1u;
+  __syncthreads();
+  const uint32_t L = sh_l;
+  if (!sh_bad) {
+    // every entry >= L, one warp per slot (entries strided over its lanes)
+    const uint32_t warp = t >> 5, lane = t & 31, nw = nt >> 5;
+    for (uint32_t q = warp; q < a.G; q += nw) {
+      const uint32_t* sl = slot(q);
+      const uint32_t m = sl[0];
+      for (uint32_t e0 = 0; e0 < m; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        const uint32_t key = e < m ? sl[2 + e] : 0u;
+        const bool keep = e < m && key >= L;
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        uint32_t base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&sh_n, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) {
+          const uint32_t d = base + __popc(bal & ((1u << lane) - 1u));
+          if (d < a.cap) {
+            a.payload[2 + d] = key;
+            a.payload[2 + a.cap + d] = (uint32_t)(sl[2 + kStSlotCap + e] + a.index_offset);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (t == 0) {
+    a.payload[0] = (sh_bad || sh_n > a.cap) ? kStBadCount : sh_n;
+    a.payload[1] = L;
   }
 }
 

@@ -1,15 +1,23 @@
 """Sharded giant-row approximate top-K.
 
 One row of n elements is cut into index-contiguous slices, one per rank
-(one process per GPU).  Each rank reduces its slice to the exact per-bucket
-stage-1 summary (atkg_stage1_summary: (2K'+2)*B uint32 words, ~16 KB for
-K'=8, B=256), the summaries are all-gathered over NCCL (NVLink/NVSwitch),
-and every rank merges them in index order and runs stage 2
-(atkg_summary_merge_top_k).  Summaries merge associatively and exactly
-(DESIGN.md section 4), so the result equals the reference's approx_top_k on
-the whole row bit for bit (topk.cpp:123-172, Stage1Accumulator::consume over
-consecutive blocks).  The only data-path collective is the summary
-all-gather: G x 16 KB, latency-bound.
+(one process per GPU).  Two exchanges, both exact (bit-identical to the
+reference's approx_top_k on the whole row, topk.cpp:238-258, which consumes
+the row's blocks in index order, Stage1Accumulator::consume, topk.cpp:123-172):
+
+* stream (default, device tensors): each rank runs the threshold stream over
+  its slice and sends a payload holding every element of the slice above the
+  slice threshold (atkg_slice_payload, a few KB); after the all-gather every
+  rank runs the per-row finish on all payloads with L = the max slice
+  threshold (atkg_payload_merge_top_k).  When the payloads cannot settle the
+  row (a gate word, the same on every rank) all ranks take:
+* exact: each rank reduces its slice to the exact per-bucket stage-1 summary
+  (atkg_stage1_summary: (2K'+2)*B uint32 words, ~16 KB for K'=8, B=256), the
+  summaries are all-gathered, merged in index order and stage 2 runs
+  (atkg_summary_merge_top_k).  Summaries merge associatively.
+The data-path collectives are these all-gathers over NCCL (NVLink/NVSwitch):
+G x a few KB, latency-bound.  atkg_sharded_approx_top_k is the same exchange
+behind the C ABI for a C++ caller with its own NCCL communicator.
 
 The reduce / merge steps are injectable so the exchange logic runs under the
 gloo backend on CPU in tests (tests/test_distributed.py) with the host
@@ -19,7 +27,8 @@ from __future__ import annotations
 
 import math
 
-from .topk import AlgoParams, stage1_summary_device, summary_merge_top_k_device, summary_words
+from .topk import (AlgoParams, payload_merge_top_k_device, slice_payload_device, slice_payload_words,
+                   stage1_summary_device, summary_merge_top_k_device, summary_words)
 
 GEN_BLOCK = 65536  # generator block of the synthetic inputs (csrc/datagen.cpp)
 
@@ -58,9 +67,14 @@ class ShardedTopK:
     before the all-gather while the others wait in it.
     """
 
-    def __init__(self, params: AlgoParams, group=None, summarize=None, merge=None):
+    def __init__(self, params: AlgoParams, group=None, summarize=None, merge=None, mode: str | None = None):
         import torch.distributed as dist
         params.validate()
+        # injected summary hooks (host emulation in tests) imply the exact exchange
+        self.mode = mode or ("exact" if summarize is not None else "stream")
+        self.fallbacks = 0
+        # gloo moves host tensors only: stage device payloads through the host
+        self._host_exchange = dist.get_backend(group) == "gloo"
         self.params = params
         self.group = group
         self.dist = dist
@@ -85,6 +99,27 @@ class ShardedTopK:
         start, length = self.bounds()
         if x_slice.numel() != length:
             raise ValueError(f"rank {self.rank} slice must hold {length} elements")
+        if self.mode == "stream":
+            import torch
+            parts = self.world
+            pw = slice_payload_words(self.params, parts)
+            if getattr(self, "_pay", None) is None or self._pay.device != x_slice.device:
+                self._pay = torch.empty(pw, dtype=torch.int32, device=x_slice.device)
+                self._pays = torch.empty(parts * pw, dtype=torch.int32, device=x_slice.device)
+                self._pst = torch.zeros(1, dtype=torch.int32, device=x_slice.device)
+            self._pst.zero_()
+            slice_payload_device(x_slice, start, self.params, parts, out=self._pay, status=self._pst)
+            if self._host_exchange and self._pay.is_cuda:
+                hp = self._pay.cpu()
+                hall = torch.empty(parts * pw, dtype=torch.int32)
+                self.dist.all_gather_into_tensor(hall, hp, group=self.group)
+                self._pays.copy_(hall)
+            else:
+                self.dist.all_gather_into_tensor(self._pays, self._pay, group=self.group)
+            v, i, gate = payload_merge_top_k_device(self._pays.view(parts, pw), self.params, status=self._pst)
+            if int(gate.item()) == 0:  # the same verdict on every rank
+                return v, i
+            self.fallbacks += 1
         w = self.words
         if self._send is None or self._send.device != x_slice.device:
             self._send = torch.empty(w + 1, dtype=torch.int32, device=x_slice.device)

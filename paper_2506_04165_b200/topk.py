@@ -465,6 +465,96 @@ def summary_merge_top_k_device(summaries: "torch.Tensor", params: AlgoParams, wa
     return (ov, oi, gv, gi) if want_grid else (ov, oi)
 
 
+def slice_payload_words(params: AlgoParams, parts: int) -> int:
+    out = C.c_size_t()
+    check(lib.atkg_slice_payload_words(C.byref(params.c()), parts, C.byref(out)))
+    return out.value
+
+
+def slice_payload_device(slice_: "torch.Tensor", index_offset: int, params: AlgoParams, parts: int, out=None,
+                         status=None):
+    """Threshold-stream payload of elements [index_offset, index_offset+len)
+    of a row sliced into `parts` (int32 words, slice_payload_words)."""
+    params.validate()
+    x = slice_.contiguous().reshape(-1)
+    dev = x.device
+    p = params.c()
+    dt = _dtype_code(x)
+    words = slice_payload_words(params, parts)
+    pay = out if out is not None else torch.empty(words, dtype=torch.int32, device=dev)
+    nbytes = C.c_size_t()
+    check(lib.atkg_slice_payload_workspace(dt, x.numel(), C.byref(p), parts, C.byref(nbytes)))
+    ws = workspace(nbytes.value, dev)
+    st = status if status is not None else _status(dev)
+    check(lib.atkg_slice_payload(dt, x.data_ptr(), x.numel(), index_offset, C.byref(p), parts, pay.data_ptr(),
+                                 ws.data_ptr(), ws.numel(), st.data_ptr(), _stream_ptr(dev)))
+    return pay
+
+
+def payload_merge_top_k_device(payloads: "torch.Tensor", params: AlgoParams, status=None):
+    """Merge `parts` slice payloads ([parts, words], index order) -> (values,
+    indices, gate).  gate (int32 device tensor) != 0: the payloads cannot
+    settle the row; take the exact summary path."""
+    params.validate()
+    s = payloads.contiguous()
+    parts = s.shape[0]
+    dev = s.device
+    k = params.global_k
+    ov = torch.empty(k, dtype=torch.float32, device=dev)
+    oi = torch.empty(k, dtype=torch.int32, device=dev)
+    gate = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = status if status is not None else _status(dev)
+    check(lib.atkg_payload_merge_top_k(s.data_ptr(), parts, C.byref(params.c()), ov.data_ptr(), oi.data_ptr(),
+                                       gate.data_ptr(), st.data_ptr(), _stream_ptr(dev)))
+    return ov, oi, gate
+
+
+class NcclComm:
+    """An NCCL communicator created by libatkg.so's own (run-time loaded)
+    NCCL, for atkg_sharded_approx_top_k.  The unique id travels by any
+    side channel (torch.distributed's store in tests)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib.atkg_nccl_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, nranks: int, uid: bytes, rank: int):
+        h = C.c_void_p()
+        check(lib.atkg_nccl_comm_init(C.byref(h), nranks, C.create_string_buffer(uid, 128), rank))
+        self.h, self.nranks, self.rank = h, nranks, rank
+
+    def close(self):
+        if self.h is not None and self.h.value:
+            check(lib.atkg_nccl_comm_destroy(self.h))
+            self.h = None
+
+
+def sharded_approx_top_k_device(slice_: "torch.Tensor", index_offset: int, params: AlgoParams, comm: NcclComm,
+                                status=None):
+    """atkg_sharded_approx_top_k: this rank's slice of one row -> the row's
+    top-K on every rank (payload exchange, exact fallback), over NCCL."""
+    params.validate()
+    x = slice_.contiguous().reshape(-1)
+    dev = x.device
+    p = params.c()
+    dt = _dtype_code(x)
+    nbytes = C.c_size_t()
+    check(lib.atkg_sharded_workspace_size(dt, x.numel(), C.byref(p), comm.nranks, C.byref(nbytes)))
+    ws = workspace(nbytes.value, dev)
+    k = params.global_k
+    ov = torch.empty(k, dtype=torch.float32, device=dev)
+    oi = torch.empty(k, dtype=torch.int32, device=dev)
+    st = status if status is not None else _status(dev)
+    check(lib.atkg_sharded_approx_top_k(dt, x.data_ptr(), x.numel(), index_offset, C.byref(p), comm.h, comm.nranks,
+                                        ov.data_ptr(), oi.data_ptr(), ws.data_ptr(), ws.numel(), st.data_ptr(),
+                                        _stream_ptr(dev)))
+    if status is None:
+        _check_device_status(st, dev)
+    return ov, oi
+
+
 # ---------------------------------------------------------------------------
 # C4: tcgen05 GEMM with stage 1 in the epilogue (mips_fused, mips.cpp:138-193)
 # ---------------------------------------------------------------------------
