@@ -23,6 +23,12 @@
  *   atkg_select_parameters        select_parameters           planner.hpp:66-67, planner.cpp:79-147
  *   atkg_fused_gemm_top_k         mips_fused semantics (stage 1 in the matmul epilogue)
  *                                 include/atk/mips.hpp:50-52, src/mips.cpp:138-193
+ *   atkg_approx_top_k_at_recall   select_parameters + PlanResult::params + approx_top_k
+ *                                 planner.hpp:38,66-67, topk.hpp:117-124
+ *   atkg_slice_payload /
+ *   atkg_payload_merge_top_k /
+ *   atkg_sharded_approx_top_k     approx_top_k of one row whose blocks live on different
+ *                                 GPUs (Stage1Accumulator::consume order, topk.hpp:68-94)
  *
  * Conventions
  *   - Device entry points take DEVICE pointers and a cudaStream_t passed as
@@ -91,9 +97,10 @@ int atkg_set_device(int device);
 /* Process-wide path-selection overrides, for tests and tuning only (no
  * effect on results: every path is bit-identical).  Unset options keep the
  * measured production choice; value UINT64_MAX resets one.  Names:
- *   no_streamthr, streamthr_force_slow, streamthr_giant_n, no_rowthr,
- *   rowthr, no_rowres, short_force_slow, no_short, fused_path (0 auto,
- *   1 unfused), sim_host_gen, no_pdl. */
+ *   no_streamthr, st_force_slow, st_giant_n (threshold stream), no_rowres,
+ *   rowthr / no_rowthr, short / no_short / short_force_slow,
+ *   rowwarp / no_rowwarp / rowwarp_force_slow (short-row kernels),
+ *   fused_path (0 auto, 1 unfused), gemm_cg, sim_host_gen, no_pdl. */
 int atkg_set_option(const char* name, uint64_t value);
 uint64_t atkg_get_option(const char* name, uint64_t dflt);
 
@@ -212,6 +219,10 @@ uint64_t atkg_accumulator_consumed(const atkg_accumulator* acc);
 /* grid [local_k][num_buckets] (device pointers), synchronises */
 int atkg_accumulator_candidates(atkg_accumulator* acc, float* d_vals, uint32_t* d_idx,
                                 void* stream);
+/* host-buffer forms (synchronous): consume() a host block (NaN rejected as
+ * in topk.cpp:126), candidates() into host arrays of num_buckets*local_k */
+int atkg_accumulator_consume_host(atkg_accumulator* acc, const float* block, uint64_t len);
+int atkg_accumulator_candidates_host(atkg_accumulator* acc, float* vals, uint32_t* idx);
 void atkg_accumulator_destroy(atkg_accumulator* acc);
 
 /* ---- fused GEMM + stage 1 (C4: x[M,Kd] . W[Kd,N] -> top-k per row) ------ */
@@ -279,6 +290,23 @@ typedef struct atkg_plan_result {
   int high_target_warning;
 } atkg_plan_result;
 int atkg_select_parameters(const atkg_plan_request* req, atkg_plan_result* out);
+
+/* approx_top_k at a recall target: the planner (select_parameters,
+ * planner.cpp:79-147) picks (K', B) from the request -- global_k = req->k,
+ * the allowed K' list, lane multiple, seed -- and the row reduction runs with
+ * them ("taking either (B, K') or (recall_target, allowed K'
+ * list), with the planner running on the host first").  Plans are memoised
+ * per request (the planner is deterministic in it).  *plan_out (optional)
+ * receives the plan used. */
+int atkg_approx_at_recall_workspace_size(int dtype, uint64_t rows, const atkg_plan_request* req,
+                                         size_t* bytes);
+int atkg_approx_top_k_at_recall(int dtype, const void* d_in, uint64_t rows,
+                                const atkg_plan_request* req, atkg_plan_result* plan_out,
+                                float* d_out_vals, uint32_t* d_out_idx, void* d_ws, size_t ws_bytes,
+                                uint32_t* d_status, void* stream);
+int atkg_approx_top_k_at_recall_host(const float* rows_in, uint64_t rows,
+                                     const atkg_plan_request* req, atkg_plan_result* plan_out,
+                                     float* out_vals, uint32_t* out_idx);
 
 /* ---- ATKV dataset container ------------------------------ */
 /* Replaces atk::read_dataset_file / write_dataset_file (dataset.hpp:45-49,

@@ -12,7 +12,7 @@ from .simulate import (SimStats, simulate_recall, simulate_recall_many, synth_di
                        synth_distinct_device, synth_distinct_row)
 from .dataset import (DatasetFormatError, VectorDataset, read_dataset_file, read_dataset_to_device,  # noqa: F401
                       write_dataset_file, write_dataset_from_device)
-from .planner import (PlanRequest, PlanResult, RecallEstimate, exact_expected_recall,  # noqa: F401
+from .planner import (PlanRequest, PlanResult, RecallEstimate, approx_top_k_at_recall, exact_expected_recall,  # noqa: F401
                       legal_bucket_counts, mc_expected_recall, mc_expected_recall_adaptive,
                       select_parameters)
 from .topk import (AlgoParams, Stage1Accumulator, TopKResult, approx_top_k, approx_top_k_batch, check_status,  # noqa: F401

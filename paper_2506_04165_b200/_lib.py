@@ -96,6 +96,12 @@ def _load():
         "atkg_mc_expected_recall_adaptive": ([P, u64, f64p, f64p, C.POINTER(C.c_uint64)], i32),
         "atkg_legal_bucket_counts": ([u64, u64, vp, u64], u64),
         "atkg_select_parameters": ([C.POINTER(PlanRequestC), C.POINTER(PlanResultC)], i32),
+        "atkg_approx_top_k_at_recall_host": ([vp, u64, C.POINTER(PlanRequestC), C.POINTER(PlanResultC), vp, vp], i32),
+        "atkg_approx_at_recall_workspace_size": ([i32, u64, C.POINTER(PlanRequestC), sz], i32),
+        "atkg_approx_top_k_at_recall": ([i32, vp, u64, C.POINTER(PlanRequestC), C.POINTER(PlanResultC), vp, vp, vp,
+                                         C.c_size_t, vp, vp], i32),
+        "atkg_accumulator_consume_host": ([vp, vp, u64], i32),
+        "atkg_accumulator_candidates_host": ([vp, vp, vp], i32),
         "atkg_dataset_read_header": ([C.c_char_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], i32),
         "atkg_dataset_read_file": ([C.c_char_p, vp, u64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], i32),
         "atkg_dataset_write_file": ([C.c_char_p, vp, u64, u64], i32),

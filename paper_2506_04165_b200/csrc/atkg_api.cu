@@ -481,14 +481,17 @@ void run_stage1_grid(int dtype, const void* in, uint64_t rows, const atkg_params
 // ---------------------------------------------------------------------------
 // stage 2 / exact selection
 // ---------------------------------------------------------------------------
+// keys per row in the radix path's buffer: k, or the pow2 >= k of the
+// global-memory sort when k exceeds one CTA's shared-memory sort
+uint64_t radix_key_stride(uint32_t k) { return k <= kMaxSortKeys ? k : next_pow2(k); }
+
 uint64_t radix_ws_bytes(uint64_t rows, uint32_t k) {
-  return align_up(rows * sizeof(RowSel)) + align_up(rows * 256 * 4) + align_up(rows * (uint64_t)k * 8);
+  return align_up(rows * sizeof(RowSel)) + align_up(rows * 256 * 4) + align_up(rows * radix_key_stride(k) * 8);
 }
 
 template <class Src>
 void run_radix(const Src& src, uint64_t rows, uint64_t count, uint32_t k, float* ov, uint32_t* oi, void* ws,
                uint32_t* status, cudaStream_t st) {
-  if (k > kMaxSortKeys) throw Unsupported("k above 16384 is not supported by the device selection path");
   char* w = static_cast<char*>(ws);
   RowSel* sel = reinterpret_cast<RowSel*>(w);
   w += align_up(rows * sizeof(RowSel));
@@ -507,8 +510,31 @@ void run_radix(const Src& src, uint64_t rows, uint64_t count, uint32_t k, float*
     radix_select_kernel<<<static_cast<unsigned>(ceil_div(rows, 8)), 256, 0, st>>>(pass, sel, hist, rows, status);
     check_launch();
   }
-  radix_gather_kernel<Src><<<grid, 256, 0, st>>>(src, sel, keys, k);
+  const uint64_t kstride = radix_key_stride(k);
+  radix_gather_kernel<Src><<<grid, 256, 0, st>>>(src, sel, keys, k, kstride);
   check_launch();
+  if (k > kMaxSortKeys) {  // global-memory bitonic network over P = kstride keys per row
+    const uint64_t P = kstride;
+    const unsigned blocks = static_cast<unsigned>(P / kSortBlock);
+    const size_t smem = kSortBlock * 8;
+    ensure_smem_fn(big_sort_block_kernel, smem);
+    ensure_smem_fn(big_sort_block_merge, smem);
+    big_sort_block_kernel<<<dim3(blocks, static_cast<unsigned>(rows)), 1024, smem, st>>>(keys, P, k);
+    check_launch();
+    for (uint64_t size = 2ull * kSortBlock; size <= P; size <<= 1) {
+      for (uint64_t stride = size >> 1; stride >= kSortBlock; stride >>= 1) {
+        const unsigned g = static_cast<unsigned>(std::min<uint64_t>(ceil_div(P / 2, 256), 4096));
+        big_sort_global_step<<<dim3(g, static_cast<unsigned>(rows)), 256, 0, st>>>(keys, P, size, stride);
+        check_launch();
+      }
+      big_sort_block_merge<<<dim3(blocks, static_cast<unsigned>(rows)), 1024, smem, st>>>(keys, P, size);
+      check_launch();
+    }
+    const unsigned eg = static_cast<unsigned>(std::min<uint64_t>(ceil_div(rows * k, 256), 65535));
+    big_sort_emit<<<eg, 256, 0, st>>>(keys, P, k, rows, ov, oi, status);
+    check_launch();
+    return;
+  }
   const uint32_t P = next_pow2(k);
   ensure_smem_fn(sort_emit_kernel, kMaxSortKeys * 8);
   sort_emit_kernel<<<static_cast<unsigned>(rows), std::min<uint32_t>(1024, P / 2), P * 8, st>>>(keys, k, P, ov, oi,
@@ -853,6 +879,64 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
   });
 }
 
+}  // extern "C"
+
+namespace atkg {
+
+// select_parameters is deterministic in its request (seed included) and runs
+// an adaptive Monte Carlo sweep: memoise the plans of recent requests
+atkg_plan_result cached_plan(const atkg_plan_request& req) {
+  struct Ent {
+    uint64_t n, k, seed;
+    double target;
+    uint32_t lane;
+    std::vector<uint32_t> kps;
+    atkg_plan_result res;
+  };
+  static std::mutex mu;
+  static std::vector<Ent> memo;
+  std::vector<uint32_t> kps(req.allowed_local_k, req.allowed_local_k + req.num_allowed_local_k);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Ent& e : memo)
+      if (e.n == req.n && e.k == req.k && e.seed == req.seed && e.target == req.recall_target &&
+          e.lane == req.lane_multiple && e.kps == kps)
+        return e.res;
+  }
+  atkg_plan_result r{};
+  rethrow(atkg_select_parameters(&req, &r));
+  std::lock_guard<std::mutex> lk(mu);
+  if (memo.size() >= 32) memo.erase(memo.begin());
+  memo.push_back(Ent{req.n, req.k, req.seed, req.recall_target, req.lane_multiple, kps, r});
+  return r;
+}
+
+atkg_params plan_params(const atkg_plan_request& req, const atkg_plan_result& r) {  // PlanResult::params
+  return atkg_params{req.n, r.num_buckets, r.local_k, static_cast<uint32_t>(req.k), req.lane_multiple};
+}
+
+}  // namespace atkg
+
+extern "C" {
+
+int atkg_approx_at_recall_workspace_size(int dtype, uint64_t rows, const atkg_plan_request* req, size_t* bytes) {
+  return guarded([&] {
+    const atkg_params p = plan_params(*req, cached_plan(*req));
+    *bytes = ws_need(ATKG_OP_APPROX, dtype, rows, p);
+  });
+}
+
+int atkg_approx_top_k_at_recall(int dtype, const void* d_in, uint64_t rows, const atkg_plan_request* req,
+                                atkg_plan_result* plan_out, float* d_out_vals, uint32_t* d_out_idx, void* d_ws,
+                                size_t ws_bytes, uint32_t* d_status, void* stream) {
+  return guarded([&] {
+    const atkg_plan_result r = cached_plan(*req);
+    if (plan_out) *plan_out = r;
+    const atkg_params p = plan_params(*req, r);
+    rethrow(atkg_approx_top_k(dtype, d_in, rows, &p, d_out_vals, d_out_idx, d_ws, ws_bytes, d_status, stream));
+  });
+}
+
 int atkg_exact_top_k(int dtype, const void* d_in, uint64_t rows, uint64_t n, uint32_t k, float* d_out_vals,
                      uint32_t* d_out_idx, void* d_ws, size_t ws_bytes, uint32_t* d_status, void* stream) {
   return guarded([&] {
@@ -1000,6 +1084,16 @@ int atkg_approx_top_k_host(const float* rows_in, uint64_t rows, const atkg_param
     CUDA_OK(cudaMemcpyAsync(out_vals, ov, no * 4, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaMemcpyAsync(out_idx, oi, no * 4, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
+  });
+}
+
+int atkg_approx_top_k_at_recall_host(const float* rows_in, uint64_t rows, const atkg_plan_request* req,
+                                     atkg_plan_result* plan_out, float* out_vals, uint32_t* out_idx) {
+  return guarded([&] {
+    const atkg_plan_result r = cached_plan(*req);
+    if (plan_out) *plan_out = r;
+    const atkg_params p = plan_params(*req, r);
+    rethrow(atkg_approx_top_k_host(rows_in, rows, &p, out_vals, out_idx));
   });
 }
 
@@ -1177,6 +1271,37 @@ int atkg_accumulator_candidates(atkg_accumulator* a, float* d_vals, uint32_t* d_
       CUDA_OK(cudaMemcpyAsync(d_idx, a->gi, kp * B * 4, cudaMemcpyDeviceToDevice, st));
     }
     check_status_sync(a->status, st);
+  });
+}
+
+int atkg_accumulator_consume_host(atkg_accumulator* a, const float* block, uint64_t len) {
+  return guarded([&] {
+    if (a->consumed + len > a->p.n) throw_inval("stage 1 fed more than n elements");
+    for (uint64_t i = 0; i < len; ++i)  // topk.cpp:126: NaN is rejected up front
+      if (block[i] != block[i]) throw NanInput();
+    if (len == 0) return;
+    HostCtx& c = host_ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    cudaStream_t st = c.s();
+    float* d = static_cast<float*>(c.get(0, len * 4));
+    CUDA_OK(cudaMemcpyAsync(d, block, len * 4, cudaMemcpyHostToDevice, st));
+    rethrow(atkg_accumulator_consume(a, ATKG_F32, d, len, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+  });
+}
+
+int atkg_accumulator_candidates_host(atkg_accumulator* a, float* vals, uint32_t* idx) {
+  return guarded([&] {
+    HostCtx& c = host_ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    cudaStream_t st = c.s();
+    const uint64_t g = a->p.num_buckets * (uint64_t)a->p.local_k;
+    float* dv = static_cast<float*>(c.get(1, g * 4));
+    uint32_t* di = static_cast<uint32_t*>(c.get(2, g * 4));
+    rethrow(atkg_accumulator_candidates(a, dv, di, st));
+    CUDA_OK(cudaMemcpyAsync(vals, dv, g * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(idx, di, g * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
   });
 }
 

@@ -164,7 +164,7 @@ __global__ void radix_select_kernel(int pass, RowSel* sel, uint32_t* hist, uint6
 }
 
 template <class Src>
-__global__ void radix_gather_kernel(Src src, RowSel* sel, uint64_t* keys, uint32_t k) {
+__global__ void radix_gather_kernel(Src src, RowSel* sel, uint64_t* keys, uint32_t k, uint64_t kstride) {
   const uint64_t row = blockIdx.y;
   const uint32_t tu = sel[row].thr_u, ti = sel[row].thr_i;
   const uint64_t n = src.count();
@@ -176,7 +176,7 @@ __global__ void radix_gather_kernel(Src src, RowSel* sel, uint64_t* keys, uint32
     if (!src.get(row, c, u, ix, nan)) continue;
     if (u < tu || (u == tu && ix <= ti)) {
       const uint32_t slot = atomicAdd(&sel[row].taken, 1u);
-      if (slot < k) keys[row * k + slot] = ((uint64_t)u << 32) | ix;
+      if (slot < k) keys[row * kstride + slot] = ((uint64_t)u << 32) | ix;
     }
   }
 }
@@ -192,6 +192,76 @@ __global__ void sort_emit_kernel(const uint64_t* keys, uint32_t k, uint32_t P, f
   for (uint32_t t = threadIdx.x; t < k; t += blockDim.x) {
     out_v[row * k + t] = __uint_as_float(key_value_bits(s[t]));
     out_i[row * k + t] = (uint32_t)s[t];
+  }
+}
+
+// ---- k above one CTA's shared memory (k > 16384): a bitonic network over
+// the row's P = pow2 >= k keys in global memory, [rows][P] padded with ~0.
+// Blocks of kSortBlock keys are sorted in shared memory (alternating
+// direction, as the network has it after every size <= kSortBlock); each
+// larger size then takes global compare-exchange steps down to stride
+// kSortBlock and one shared-memory pass for the smaller strides.
+constexpr uint32_t kSortBlock = 16384;
+
+__global__ void big_sort_block_kernel(uint64_t* keys, uint64_t P, uint32_t k) {
+  extern __shared__ uint64_t sb[];
+  const uint64_t row = blockIdx.y, base = (uint64_t)blockIdx.x * kSortBlock;
+  uint64_t* g = keys + row * P + base;
+  for (uint32_t c = threadIdx.x; c < kSortBlock; c += blockDim.x) sb[c] = base + c < k ? g[c] : ~0ull;
+  __syncthreads();
+  const bool desc = (blockIdx.x & 1u) != 0;
+  for (uint32_t size = 2; size <= kSortBlock; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t t = threadIdx.x; t < kSortBlock / 2; t += blockDim.x) {
+        const uint32_t i = 2 * t - (t & (stride - 1)), j = i + stride;
+        const bool asc = ((i & size) == 0) != (desc && size == kSortBlock);
+        const uint64_t a = sb[i], b = sb[j];
+        if ((a > b) == asc) { sb[i] = b; sb[j] = a; }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t c = threadIdx.x; c < kSortBlock; c += blockDim.x) g[c] = sb[c];
+}
+
+__global__ void big_sort_global_step(uint64_t* keys, uint64_t P, uint64_t size, uint64_t stride) {
+  const uint64_t row = blockIdx.y;
+  uint64_t* g = keys + row * P;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < P / 2; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = 2 * t - (t & (stride - 1)), j = i + stride;
+    const bool asc = (i & size) == 0;
+    const uint64_t a = g[i], b = g[j];
+    if ((a > b) == asc) { g[i] = b; g[j] = a; }
+  }
+}
+
+__global__ void big_sort_block_merge(uint64_t* keys, uint64_t P, uint64_t size) {
+  extern __shared__ uint64_t sb[];
+  const uint64_t row = blockIdx.y, base = (uint64_t)blockIdx.x * kSortBlock;
+  uint64_t* g = keys + row * P + base;
+  for (uint32_t c = threadIdx.x; c < kSortBlock; c += blockDim.x) sb[c] = g[c];
+  __syncthreads();
+  const bool asc = (base & size) == 0;
+  for (uint32_t stride = kSortBlock >> 1; stride > 0; stride >>= 1) {
+    for (uint32_t t = threadIdx.x; t < kSortBlock / 2; t += blockDim.x) {
+      const uint32_t i = 2 * t - (t & (stride - 1)), j = i + stride;
+      const uint64_t a = sb[i], b = sb[j];
+      if ((a > b) == asc) { sb[i] = b; sb[j] = a; }
+    }
+    __syncthreads();
+  }
+  for (uint32_t c = threadIdx.x; c < kSortBlock; c += blockDim.x) g[c] = sb[c];
+}
+
+__global__ void big_sort_emit(const uint64_t* keys, uint64_t P, uint32_t k, uint64_t rows, float* out_v,
+                              uint32_t* out_i, const uint32_t* status) {
+  if (*status) return;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rows * k;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t row = t / k, c = t - row * k;
+    const uint64_t key = keys[row * P + c];
+    out_v[t] = __uint_as_float(key_value_bits(key));
+    out_i[t] = (uint32_t)key;
   }
 }
 

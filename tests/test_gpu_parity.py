@@ -331,3 +331,61 @@ def test_select_candidates_rank_path_vs_port(cuda, port, count):
                     continue
                 r = atk.select_top_k_candidates(v, i, k, lim)
                 assert np.array_equal(bits(r.values), bits(pv)) and np.array_equal(r.indices, pi)
+
+
+# ---- k above one CTA's shared-memory sort (the reference takes any k <= n) ----
+@pytest.mark.parametrize("n,k", [(1 << 18, 20000), (1 << 20, 65536), (100000, 16385)])
+def test_exact_top_k_large_k(cuda, ref, n, k):
+    import paper_2506_04165_b200 as atk
+    x = np.random.default_rng(k).standard_normal((2, n)).astype(np.float32)
+    x[1, ::7] = np.round(x[1, ::7])  # ties
+    v, i = atk.exact_top_k_device(torch.from_numpy(x).to(cuda), k)
+    for r in range(2):
+        ev, ei = ref.exact_top_k(x[r], k)
+        assert np.array_equal(bits(v[r]), bits(ev)) and np.array_equal(u32(i[r]), ei)
+
+
+@pytest.mark.parametrize("n,B,kp,k", [(1 << 20, 8192, 4, 20000), (1 << 19, 16384, 2, 32768)])
+def test_approx_top_k_large_k(cuda, ref, n, B, kp, k):
+    import paper_2506_04165_b200 as atk
+    x = np.random.default_rng(n + k).standard_normal((2, n)).astype(np.float32)
+    v, i = atk.approx_top_k_device(torch.from_numpy(x).to(cuda), atk.AlgoParams(n, B, kp, k))
+    rv, ri = ref.approx_top_k_batch(x, B, kp, k)
+    assert np.array_equal(bits(v), bits(rv)) and np.array_equal(u32(i), ri)
+
+
+def test_select_candidates_large_k(cuda, ref):
+    import paper_2506_04165_b200 as atk
+    rng = np.random.default_rng(5)
+    vals = rng.standard_normal(50000).astype(np.float32)
+    vals[::5] = 1.0
+    idx = rng.permutation(200000)[:50000].astype(np.uint32)
+    ov, oi = atk.select_candidates_device(torch.from_numpy(vals).to(cuda)[None, :],
+                                          torch.from_numpy(idx.view(np.int32)).to(cuda)[None, :], 30000,
+                                          index_limit=150000)
+    rv, ri = ref.select_candidates(vals, idx, 30000, 150000)
+    assert np.array_equal(bits(ov[0]), bits(rv)) and np.array_equal(u32(oi[0]), ri)
+
+
+@pytest.mark.parametrize("target,kps", [(0.95, (1, 2, 4, 8)), (0.99, (2,))])
+def test_approx_top_k_at_recall(cuda, ref, target, kps):
+    """Recall target in: the plan equals the reference planner's
+    and the rows equal the reference approx_top_k_batch with that plan."""
+    import paper_2506_04165_b200 as atk
+    from paper_2506_04165_b200 import data
+    n, k, rows = 14336, 287, 32
+    req = atk.PlanRequest(n, k, target, list(kps), 128, 0)
+    pl = ref.select_parameters(n, k, target, kps, 128, 0)
+    x = data.normal_f32(77, (rows, n))
+    plan, res = atk.approx_top_k_at_recall(x, rows, req)
+    assert (plan.local_k, plan.num_buckets) == (pl.local_k, pl.num_buckets)
+    assert plan.estimated_recall.value == pl.recall
+    rv, ri = ref.approx_top_k_batch(x, pl.num_buckets, pl.local_k, k)
+    for r in range(rows):
+        assert np.array_equal(bits(res[r].values), bits(rv[r])) and np.array_equal(u32(res[r].indices), ri[r])
+    bits16, f = data.normal_bf16(78, (rows, n))
+    xd = torch.from_numpy(bits16.view(np.int16)).to(cuda).view(torch.bfloat16)
+    plan2, (v, i) = atk.approx_top_k_at_recall(xd, rows, req)
+    rv, ri = ref.approx_top_k_batch(f, pl.num_buckets, pl.local_k, k)
+    assert plan2.num_buckets == pl.num_buckets
+    assert np.array_equal(bits(v), bits(rv)) and np.array_equal(u32(i), ri)
