@@ -111,6 +111,17 @@ RwPlan plan_rowwarp(int dtype, const void* in, uint64_t rows, uint64_t n, uint64
 void run_rowwarp(const RwPlan& rp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
                  float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
 
+// one warp per bf16 row streamed once into registers, B = 128, K' = 4 (rowreg.cu)
+struct RgPlan {
+  bool ok = false;
+  uint32_t S = 0, warps = 0, sub_shift = 0, grid = 0;
+  size_t smem = 0;
+};
+RgPlan plan_rowreg(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
+                   bool for_size = false);
+void run_rowreg(const RgPlan& rp, const void* in, uint64_t rows, uint32_t k, float* ov, uint32_t* oi,
+                uint32_t* status, cudaStream_t st);
+
 // stage 2 by counting-sort ranks for 128 < count <= 1024 (streamthr.cu);
 // false if not applicable
 bool run_select_ranked(const float* vals, const uint32_t* idx, uint64_t rows, uint64_t count, uint64_t stride,

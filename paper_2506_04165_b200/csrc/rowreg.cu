@@ -1,0 +1,80 @@
+// rowreg.cu -- host planner + launcher of row_reg_kernel (rowreg.cuh), the
+// approx_top_k path for short bf16 rows with B = 128, K' = 4 (config C3).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "internal.hpp"
+#include "rowreg.cuh"
+
+namespace atkg {
+
+namespace {
+
+template <int S, int NW>
+void rg_launch(const RgPlan& rp, const RgArgs& a, cudaStream_t st) {
+  auto kern = row_reg_kernel<S, NW>;
+  ensure_smem_fn(kern, rp.smem);
+  kern<<<rp.grid, 32 * NW, rp.smem, st>>>(a);
+  check_launch();
+}
+
+template <int S>
+void rg_dispatch(const RgPlan& rp, const RgArgs& a, cudaStream_t st) {
+  switch (rp.warps) {
+    case 8: rg_launch<S, 8>(rp, a, st); break;
+    case 12: rg_launch<S, 12>(rp, a, st); break;
+    case 16: rg_launch<S, 16>(rp, a, st); break;
+    case 20: rg_launch<S, 20>(rp, a, st); break;
+    default: rg_launch<S, 22>(rp, a, st); break;
+  }
+}
+
+}  // namespace
+
+RgPlan plan_rowreg(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
+                   bool for_size) {
+  RgPlan rp;
+  // default for its shapes; the explicit opt-ins of the other row kernels win
+  if (!for_size && (!opt("rowreg", 1) || opt("short", 0) || opt("rowwarp", 0))) return rp;
+  if (dtype != ATKG_BF16 || B != 128 || kp != 4 || n % 128 != 0) return rp;
+  const uint64_t S = n / 128;
+  if (S != 28 && S != 56 && S != 112 && S != 128) return rp;  // instantiated row lengths
+  if (k > kRgTmp || (uint64_t)k > B * kp) return rp;
+  if (reinterpret_cast<uintptr_t>(in) % 8 != 0) return rp;
+  rp.S = (uint32_t)S;
+  uint32_t w = (uint32_t)opt("rowreg_warps", 20);
+  rp.warps = w <= 8 ? 8 : w <= 12 ? 12 : w <= 16 ? 16 : w <= 20 ? 20 : 22;
+  rp.smem = (size_t)rp.warps * kRgWarpSmem;
+  rp.sub_shift = 0;
+  while ((n - 1) >> rp.sub_shift >= 4) ++rp.sub_shift;
+  rp.grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(rows, (uint64_t)sm_count()));
+  rp.ok = true;
+  return rp;
+}
+
+void run_rowreg(const RgPlan& rp, const void* in, uint64_t rows, uint32_t k, float* ov, uint32_t* oi,
+                uint32_t* status, cudaStream_t st) {
+  RgArgs a{};
+  a.in = static_cast<const uint16_t*>(in);
+  a.rows = rows;
+  a.k = k;
+  a.sub_shift = rp.sub_shift;
+  a.margin = (uint32_t)opt("rowreg_margin", 6);
+  a.slack = (uint32_t)opt("rowreg_slack", 30);
+  a.force = (uint32_t)opt("rowreg_force", 0);
+  a.probe = (uint32_t)opt("rowreg_probe", 0);
+  a.out_v = ov;
+  a.out_i = oi;
+  a.status = status;
+  g_prof.bracket_begin(st);
+  switch (rp.S) {
+    case 28: rg_dispatch<28>(rp, a, st); break;
+    case 56: rg_dispatch<56>(rp, a, st); break;
+    case 112: rg_dispatch<112>(rp, a, st); break;
+    default: rg_dispatch<128>(rp, a, st); break;
+  }
+  g_prof.bracket_end(st);
+}
+
+}  // namespace atkg

@@ -1,0 +1,62 @@
+"""Device timing of row_reg_kernel (csrc/rowreg.cuh) on the C3 shape: CTA
+sizes, phase probes, the forced two-pass path and the previous default
+(row_resident_kernel).  Development aid: CUDA events on the current stream,
+inputs > L2."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2506_04165_b200 as atk  # noqa: E402
+
+opt = atk._lib.option
+
+
+def timeit(fn, iters=50, warm=5):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters * 1e3  # us
+
+
+def main():
+    rows, n, k = 8192, 14336, 287
+    dev = torch.device("cuda:0")
+    x = torch.randn(rows, n, device=dev).to(torch.bfloat16)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    out = (torch.empty(rows, k, device=dev), torch.empty(rows, k, dtype=torch.int32, device=dev))
+    p = atk.AlgoParams(n, 128, 4, k)
+    run = lambda: atk.approx_top_k_device(x, p, status=st, out=out)  # noqa: E731
+    byts = rows * n * 2
+
+    def line(what, t):
+        print(f"{what:44s} {t:7.1f} us  {byts / t / 1e3:6.0f} GB/s  {byts / t / 1e3 / 6552.3:.3f} of peak", flush=True)
+
+    warps = [int(a) for a in sys.argv[1:] if a.isdigit()] or [8, 12, 16, 20, 22]
+    for w in warps:
+        with opt("rowreg_warps", w):
+            line(f"rowreg warps={w}", timeit(run))
+            if "--probe" in sys.argv:
+                for pr, what in [(1, "stream"), (2, "+ check/bisect"), (3, "+ list"), (4, "+ values"), (5, "+ crowded")]:
+                    with opt("rowreg_probe", pr):
+                        line(f"  warps={w} probe {pr} ({what})", timeit(run))
+            with opt("rowreg_force", 1):
+                line(f"  warps={w} every row two-pass", timeit(run))
+    if "--sweep" in sys.argv:
+        for m, s in [(2, 30), (6, 10), (6, 60), (12, 30), (3, 20)]:
+            with opt("rowreg_margin", m), opt("rowreg_slack", s):
+                line(f"margin={m} slack={s}", timeit(run))
+    with opt("rowreg", 0):
+        line("row_resident_kernel (previous default)", timeit(run, iters=20))
+    atk.check_status(st)
+
+
+if __name__ == "__main__":
+    main()
