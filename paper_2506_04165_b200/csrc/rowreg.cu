@@ -60,8 +60,8 @@ void run_rowreg(const RgPlan& rp, const void* in, uint64_t rows, uint32_t k, flo
   a.rows = rows;
   a.k = k;
   a.sub_shift = rp.sub_shift;
-  a.margin = (uint32_t)opt("rowreg_margin", 6);
-  a.slack = (uint32_t)opt("rowreg_slack", 30);
+  a.margin = (uint32_t)opt("rowreg_margin", 5);
+  a.starters = (uint32_t)std::max<uint64_t>(1, opt("rowreg_starters", 4));
   a.force = (uint32_t)opt("rowreg_force", 0);
   a.probe = (uint32_t)opt("rowreg_probe", 0);
   a.out_v = ov;

@@ -4,36 +4,38 @@
 //
 // The earlier row kernels (rowres, rowwarp, shortrow) stage whole rows in
 // shared memory; 28 KB per row leaves 6-8 rows (warps) per SM and they end
-// up latency-bound.  Here the row never touches shared memory:
+// up latency-bound.  Here a row only passes through a 4 KB staging tile:
 //   * lane l reads its own 8 bytes (buckets 4l..4l+3, topk.hpp:13-15: element
 //     i goes to bucket i mod B) of every stride-row straight into registers
-//     (256 B per warp load, 14 loads in flight per lane, double-buffered);
-//   * per bf16x2 word one packed max (the group maxima) and one packed
-//     compare + mask-or (the hit map) -- 7 instructions per 4 elements and
-//     lane, no branch, no per-bucket state in the loop;
-//   * the hit map of a lane's 4 buckets (<= 128 stride-rows each) stays in
-//     14 registers.
-// Threshold argument (shortrow.cuh): split every bucket's
-// stride-rows into K' disjoint groups.  If at least K of the B K' group
-// maxima are >= L then M = sum_b min(K', c_b(L)) >= K, so the top K of the
-// row's candidates are the top K of its candidates >= L, and those follow
-// from the elements >= L alone (Alg. 1 over a bucket's elements >= L,
-// topk.cpp:80-102, the S* lemma).
-//   fast path   L0 = the warp's prediction (the previous row's exact level
-//               minus a margin, then a +-1 code controller on the count of
-//               group maxima >= L0).  Maxima and hit map come from the same
-//               pass; the count proves M >= K afterwards.  Any L0 is exact.
-//   two-pass    no prediction yet, or the count fell short: bisect the exact
-//               K-th largest group maximum (16 packed-compare rounds), then
-//               a second compare-only pass (the row is in L2).
-//   exact path  L = -inf, or more hits than the list holds (ties at L):
-//               Alg. 1 of every bucket as the reference runs it, then a
-//               bitonic sort of the B K' rank keys.  Slow, degenerate rows only.
-// After the stream: hits -> list (bucket-major, position-ascending inside a
-// bucket), values fetched in balanced rounds (scattered 2-byte loads, L2),
-// crowded buckets (c_b > K') resolved by Alg. 1 over their hits with one lane
-// per crowded bucket, then the same (value code, index quarter) counting
-// sort as rowwarp.cuh for the first K in output order (topk.cpp:30-50).
+//     (256 B per warp load, 16 loads in flight per lane, double-buffered);
+//   * per bf16x2 word one packed 3-input max (the group maxima, two words
+//     per instruction) and one packed compare + mask-or (the hit map): no
+//     branch, no per-bucket state in the loop;
+//   * every 16 stride-rows the lane walks the set bits of its hit map and
+//     copies the hits (value | position) from its own column of the staging
+//     tile to its log -- the row is never read again.
+// Threshold argument: for a level L let c_b = the elements of
+// bucket b that are >= L and M = sum_b min(K', c_b).  If M >= K the top K of
+// the row's candidates are the top K of its candidates >= L, and those
+// follow from the elements >= L alone (Alg. 1 over a bucket's elements >= L,
+// topk.cpp:80-102, the S* lemma).  M is known exactly after the pass (the
+// popcounts of the hit map), so ANY level may be tried:
+//   fast path   L0 = the CTA's prediction: the level of the K-th candidate of
+//               the row finished last (a by-product of its stage 2) minus a
+//               margin.  One pass; M >= K afterwards proves it.
+//   two-pass    no prediction yet, M < K, or a lane's log overflowed: the
+//               exact K-th largest of the B K' group maxima (K' disjoint groups
+//               of stride-rows per bucket; 16 packed-compare rounds on the
+//               maxima the first pass kept) guarantees M >= K; a second pass
+//               (the row is in L2) logs the hits against it.
+//   exact path  L = -inf, or a log overflows even then (ties at L, one
+//               bucket holding the large values): Alg. 1 of every bucket as
+//               the reference runs it, then a bitonic sort of the B K' rank
+//               keys.  Slow; degenerate rows only.
+// After the pass: crowded buckets (c_b > K') are resolved by Alg. 1 over
+// their logged hits (one lane per crowded bucket), then the (value code,
+// index quarter) counting sort of rowwarp.cuh writes the first K in output
+// order (topk.cpp:30-50).
 #pragma once
 
 #include <cuda_bf16.h>
@@ -43,21 +45,20 @@
 
 namespace atkg {
 
-constexpr uint32_t kRgCap = 1024;            // hit list entries per row
 constexpr uint32_t kRgBins = 1024;           // 256 value codes x 4 index quarters
-constexpr uint32_t kRgTmp = 512;             // candidates after the crowded buckets: <= B K'
-constexpr uint32_t kRgDead = 0xffffffffu;    // dropped list entry (sorts last)
+constexpr uint32_t kRgTmp = 512;             // candidates: <= B K'
 constexpr uint32_t kRgKeyNegInf = 0x007fu;   // asc_code16(-inf)
-constexpr uint32_t kRgWarpSmem = 4 * kRgCap + 4 * kRgTmp + 4 * kRgBins;  // E | tmp | bins
-constexpr int kRgBatch = 14;                 // stride-rows per load batch
+constexpr int kRgTile = 8;                   // stride-rows per load batch = per staging tile
+// per warp: staging tile [8][32] x 8 B | state [128 buckets][4] u32 | bins | tmp
+constexpr uint32_t kRgWarpSmem = kRgTile * 256 + 4 * 512 + 4 * kRgBins + 4 * kRgTmp;
 
 struct RgArgs {
   const uint16_t* in;
   uint64_t rows;
   uint32_t k;
   uint32_t sub_shift;   // pos >> sub_shift < 4
-  uint32_t margin;      // prediction: codes below the last exact level
-  uint32_t slack;       // controller: aim at K + slack group maxima >= L0
+  uint32_t margin;      // prediction: codes below the level of the last row's K-th candidate
+  uint32_t starters;    // warps per CTA that start without a prediction (the rest wait for one)
   uint32_t force;       // tests: 1 = every row two-pass, 2 = every row exact, 3 = sort instead of bins
   uint32_t probe;       // development: stop after phase `probe`
   float* out_v;
@@ -116,29 +117,40 @@ __host__ __device__ constexpr int rg_group(int s) {
   return g;
 }
 
-// One pass over the row: lane-local group maxima (MAX) and the hit map
-// against L2 (acc[w][q]: half h of word w = bucket 4 lane + 2 w + h, bit i =
-// stride-row 16 q + i).
-template <int S, bool MAX>
-__device__ __forceinline__ void rg_stream(const uint2* p, uint32_t L2, uint32_t (&acc)[2][(S + 15) / 16],
+// One pass over the row: lane-local group maxima (MAX) and Alg. 1
+// (topk.cpp:80-102) over the hits of each of the lane's 4 buckets, in stream
+// order.  Per tile of 8 stride-rows: the loads (issued one tile ahead) are
+// compared against L2 and copied to the lane's column of the staging tile;
+// bit 8 u + 7 - i of the tile's hit mask = element slot u of stride-row i
+// (u = 0, 1, 2, 3 <-> bucket 4 lane + 0, 2, 1, 3); the lane then walks the
+// set bits from the top (ascending stride-row inside a slot) and inserts
+// (code << 16 | position) into the bucket's state[4], kept in Alg. 1 order
+// (value descending, a later equal element never passes an earlier one; the
+// empty slots are 0, below every hit).  POS: the hits are strictly positive,
+// their bf16 bits order as they are; otherwise ascending codes.
+template <int S, bool MAX, bool POS>
+__device__ __forceinline__ void rg_stream(const uint2* p, uint32_t L2, uint32_t lane, uint2* stage, uint4* state,
                                           uint32_t (&gm)[2][4]) {
-  constexpr int NB = (S + kRgBatch - 1) / kRgBatch;
-  uint2 buf[2][kRgBatch];
+  constexpr int NB = (S + kRgTile - 1) / kRgTile;
+  uint2 buf[2][kRgTile];
 #pragma unroll
-  for (int i = 0; i < kRgBatch; ++i)
+  for (int i = 0; i < kRgTile; ++i)
     if (i < S) buf[0][i] = rg_ldg(p + i * 32);
+  const uint8_t* col = reinterpret_cast<const uint8_t*>(stage + lane);
+  uint4* st4 = state + 4 * lane;  // the lane's buckets 4 lane .. 4 lane + 3
 #pragma unroll
   for (int bt = 0; bt < NB; ++bt) {
     if (bt + 1 < NB) {
 #pragma unroll
-      for (int i = 0; i < kRgBatch; ++i) {
-        const int s = (bt + 1) * kRgBatch + i;
+      for (int i = 0; i < kRgTile; ++i) {
+        const int s = (bt + 1) * kRgTile + i;
         if (s < S) buf[(bt + 1) & 1][i] = rg_ldg(p + s * 32);
       }
     }
+    uint32_t m = 0;
 #pragma unroll
-    for (int i = 0; i < kRgBatch; ++i) {
-      const int s = bt * kRgBatch + i;
+    for (int i = 0; i < kRgTile; ++i) {
+      const int s = bt * kRgTile + i;
       if (s < S) {
         const uint2 v = buf[bt & 1][i];
         if (MAX) {
@@ -146,9 +158,28 @@ __device__ __forceinline__ void rg_stream(const uint2* p, uint32_t L2, uint32_t 
           gm[0][g] = bmax_nan(gm[0][g], v.x);
           gm[1][g] = bmax_nan(gm[1][g], v.y);
         }
-        const uint32_t bit = 0x00010001u << (s & 15);
-        acc[0][s >> 4] |= rg_ge(v.x, L2) & bit;
-        acc[1][s >> 4] |= rg_ge(v.y, L2) & bit;
+        m |= rg_ge(v.x, L2) & (0x00010001u << (7 - i));
+        m |= rg_ge(v.y, L2) & (0x01000100u << (7 - i));
+        stage[(7 - i) * 32 + lane] = v;
+      }
+    }
+    while (m) {
+      const uint32_t b = 31u - (uint32_t)__clz((int)m);
+      m ^= 1u << b;
+      const uint32_t r = b & 7u, u = b >> 3;           // stride-row bt * 8 + 7 - r, element slot u
+      const uint32_t j = ((u & 1u) << 1) | (u >> 1);    // bucket 4 lane + j
+      uint32_t val = *reinterpret_cast<const uint16_t*>(col + r * 256 + j * 2);
+      if (!POS) val = asc_code16(val);
+      const uint32_t e = (val << 16) | (((bt * kRgTile + 7) << 7) - (r << 7) + 4 * lane + j);
+      uint4 sv = st4[j];
+      if (sv.w <= (e | 0xffffu)) {  // value >= v[K' - 1]: e replaces the minimum slot, then rises
+        const uint32_t eb = e & 0xffff0000u;  // past the strictly smaller values
+        const bool a2 = sv.z >= eb, a1 = sv.y >= eb, a0 = sv.x >= eb;  // slot k stays above e
+        sv.w = a2 ? e : sv.z;
+        sv.z = a2 ? sv.z : (a1 ? e : sv.y);
+        sv.y = a1 ? sv.y : (a0 ? e : sv.x);
+        sv.x = a0 ? sv.x : e;
+        st4[j] = sv;
       }
     }
   }
@@ -209,24 +240,34 @@ __device__ __noinline__ void rg_exact(const uint16_t* xr, uint32_t lane, uint32_
 
 // S = stride-rows (n = 128 S <= 16384), B = 128, K' = 4.  One CTA per SM;
 // CTA c owns the rows [rows c / G, rows (c + 1) / G) and its warps pull them
-// from a shared counter.
+// from a shared counter.  `pred` is the CTA's prediction (an ascending code;
+// 0 = none yet, ~0 = the starters found none).
 template <int S, int NW>
 __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
-  constexpr int NQ = (S + 15) / 16;
   constexpr uint32_t n = 128u * S;
   extern __shared__ __align__(128) uint8_t rg_smem[];
   __shared__ uint32_t queue;
+  __shared__ volatile uint32_t pred;
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t K = a.k;
-  uint32_t* E = reinterpret_cast<uint32_t*>(rg_smem + (size_t)wid * kRgWarpSmem);
-  uint32_t* tmp = E + kRgCap;
-  uint32_t* bins = tmp + kRgTmp;
+  uint8_t* wsm = rg_smem + (size_t)wid * kRgWarpSmem;
+  uint2* stage = reinterpret_cast<uint2*>(wsm);
+  uint4* state = reinterpret_cast<uint4*>(wsm + kRgTile * 256);
+  uint32_t* cand = reinterpret_cast<uint32_t*>(state);  // [bucket][4], 0 = empty
+  uint32_t* bins = cand + 512;
+  uint32_t* tmp = bins + kRgBins;
   const uint64_t r0 = a.rows * blockIdx.x / gridDim.x, r1 = a.rows * (blockIdx.x + 1) / gridDim.x;
   const uint32_t nrows = (uint32_t)(r1 - r0);
-  if (threadIdx.x == 0) queue = 0;
+  if (threadIdx.x == 0) {
+    queue = 0;
+    pred = 0;
+  }
   __syncthreads();
   const uint32_t lt = (1u << lane) - 1u;
-  uint32_t L0key = 0;  // 0 = no prediction yet
+  // every warp but the starters waits for the first prediction
+  if (wid >= a.starters && a.force == 0) {
+    while (pred == 0) __nanosleep(500);
+  }
 
 #pragma unroll 1
   for (;;) {
@@ -240,28 +281,34 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
     float* ov = a.out_v + row * K;
     uint32_t* oi = a.out_i + row * K;
 
-    // ---- the stream: group maxima + hit map against the prediction ------
-    uint32_t acc[2][NQ], gm[2][4];
+    // ---- the pass: group maxima + Alg. 1 over the hits against the prediction
+    uint32_t gm[2][4];
 #pragma unroll
-    for (int w = 0; w < 2; ++w) {
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) acc[w][q] = 0;
+    for (int w = 0; w < 2; ++w)
 #pragma unroll
       for (int g = 0; g < 4; ++g) gm[w][g] = 0xff80ff80u;
+    auto clear_state = [&]() {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) state[4 * lane + j] = make_uint4(0, 0, 0, 0);
+    };
+    clear_state();
+    uint32_t Lkey = pred;
+    const bool have = Lkey != 0 && Lkey != 0xffffffffu && a.force == 0;
+    bool posmode = have && Lkey > 0x8000u;
+    if (have) {
+      if (posmode) rg_stream<S, true, true>(p, rg_bits2(Lkey), lane, stage, state, gm);
+      else rg_stream<S, true, false>(p, rg_bits2(Lkey), lane, stage, state, gm);
+    } else {
+      rg_stream<S, true, true>(p, 0x7fc07fc0u, lane, stage, state, gm);  // NaN level: maxima only
     }
-    const bool have = L0key != 0 && a.force == 0;
-    uint32_t L2 = have ? rg_bits2(L0key) : 0x7fc07fc0u;  // NaN: no hits, count 0
-    rg_stream<S, true>(p, L2, acc, gm);
-    if (a.probe == 1) {  // development: the stream alone (its results consumed)
-      uint32_t z = 0;
+    if (a.probe == 1) {  // development: the pass alone (its results consumed)
+      uint32_t z = state[4 * lane].x;
 #pragma unroll
-      for (int w = 0; w < 2; ++w) {
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) z ^= acc[w][q];
+      for (int w = 0; w < 2; ++w)
 #pragma unroll
         for (int g = 0; g < 4; ++g) z += gm[w][g];
-      }
       if (z == 0x12345u) oi[lane] = z;
+      if (pred == 0) pred = 0xbff0u;
       continue;
     }
 
@@ -272,43 +319,25 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
     const uint32_t nan = ((mlo & 0x7fffu) > 0x7f80u || (mhi & 0x7fffu) > 0x7f80u) ? 1u : 0u;
     if (__reduce_or_sync(0xffffffffu, nan)) {
       if (lane == 0) atomicOr(a.status, ATKG_FLAG_NAN);
+      if (pred == 0) pred = 0xffffffffu;
       continue;
     }
     const uint32_t kmax = __reduce_max_sync(0xffffffffu, max(asc_code16(mlo), asc_code16(mhi)));
 
-    // hit maps per bucket (bit r of bm[j][t] = stride-row 32 t + r), counts,
-    // list offsets; H = hits of the row
-    uint32_t bm[4][4], c[4], H = 0, d = 0;
-    auto bucket_maps = [&]() {
-      uint32_t nl = 0;
+    // M = sum_b min(K', c_b) = the filled slots
+    auto filled = [&]() {
+      uint32_t f = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        c[j] = 0;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const uint32_t lo = 2 * t < NQ ? acc[j >> 1][2 * t < NQ ? 2 * t : 0] : 0u;
-          const uint32_t hi = 2 * t + 1 < NQ ? acc[j >> 1][2 * t + 1 < NQ ? 2 * t + 1 : 0] : 0u;
-          bm[j][t] = __byte_perm(lo, hi, (j & 1) ? 0x7632 : 0x5410);
-          c[j] += __popc(bm[j][t]);
-        }
-        nl += c[j];
+        const uint4 sv = state[4 * lane + j];
+        f += (sv.x ? 1u : 0u) + (sv.y ? 1u : 0u) + (sv.z ? 1u : 0u) + (sv.w ? 1u : 0u);
       }
-      d = rg_excl_scan(nl, lane, &H);
+      return __reduce_add_sync(0xffffffffu, f);
     };
-
-    uint32_t Lkey = L0key;
+    uint32_t M = have ? filled() : 0u;
     bool exact = a.force == 2;
-    const uint32_t cnt = have ? __reduce_add_sync(0xffffffffu, rg_count_ge(gm, L2)) : 0u;
-    bool twopass = !have || cnt < K;
-    if (!twopass) {
-      bucket_maps();
-      twopass = H > kRgCap;  // the prediction sits far below the row's level
-      // controller: hold the count of group maxima >= L0 near K + slack
-      if (cnt < K + a.slack / 2) L0key = max(L0key - 1, kRgKeyNegInf + 1);
-      else if (cnt > K + a.slack + a.slack / 2) L0key = L0key + 1;
-    }
-    if (twopass) {
-      // ---- the exact K-th largest group maximum, then a compare-only pass
+    if (M < K) {
+      // ---- two-pass: the exact K-th largest group maximum guarantees M >= K
       uint32_t cur = 0;
 #pragma unroll 1
       for (int bit = 15; bit >= 0; --bit) {
@@ -319,115 +348,40 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
       Lkey = cur;
       if (Lkey <= kRgKeyNegInf) {
         exact = true;
-        L0key = 0;
       } else {
-        L2 = rg_bits2(Lkey);
-#pragma unroll
-        for (int w = 0; w < 2; ++w)
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) acc[w][q] = 0;
-        rg_stream<S, false>(p, L2, acc, gm);
-        L0key = max(Lkey, kRgKeyNegInf + 1 + a.margin) - a.margin;
-        bucket_maps();
-        if (H > kRgCap) exact = true;  // ties at L
+        if (pred == 0) pred = max(Lkey, kRgKeyNegInf + 1 + a.margin) - a.margin;
+        posmode = Lkey > 0x8000u;
+        clear_state();
+        if (posmode) rg_stream<S, false, true>(p, rg_bits2(Lkey), lane, stage, state, gm);
+        else rg_stream<S, false, false>(p, rg_bits2(Lkey), lane, stage, state, gm);
+        M = filled();
       }
     }
     if (a.probe == 2) continue;
     if (exact) {
-      rg_exact<S>(xr, lane, K, reinterpret_cast<uint64_t*>(E), ov, oi);
+      if (pred == 0) pred = 0xffffffffu;
+      __syncwarp();
+      rg_exact<S>(xr, lane, K, reinterpret_cast<uint64_t*>(bins), ov, oi);
       continue;
     }
-    const bool binned = kmax - Lkey < 256u && a.force != 3;
+    __syncwarp();
+
+    // ---- stage 2: the first K of the M >= K candidates -------------------
+    const uint32_t kmaxm = posmode ? (kmax & 0x7fffu) : kmax;
+    const uint32_t Lm = posmode ? (Lkey & 0x7fffu) : Lkey;
+    const bool binned = kmaxm - Lm < 256u && a.force != 3;
+    uint32_t Lstar = Lkey;  // level of the K-th candidate (ascending code)
     if (binned) {
 #pragma unroll
       for (int i = 0; i < (int)(kRgBins / 128); ++i)
         reinterpret_cast<uint4*>(bins)[lane + 32 * i] = make_uint4(0, 0, 0, 0);
-    }
-
-    // ---- hits -> list (bucket-major, position-ascending inside a bucket),
-    //      crowded buckets -> descriptors (offset | count << 16) in tmp
-    uint32_t nov = 0;
-    {
-      uint32_t o = d;
+      __syncwarp();
+      auto bin_of = [&](uint32_t key) { return ((kmaxm - (key >> 16)) << 2) | ((key & 0xffffu) >> a.sub_shift); };
+      uint32_t keys[16];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t crowded = c[j] > 4u ? 1u : 0u;
-        const uint32_t bal = __ballot_sync(0xffffffffu, crowded);
-        if (crowded) tmp[nov + __popc(bal & lt)] = o | (c[j] << 16);
-        nov += __popc(bal);
-        o += c[j];
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t bk = 4 * lane + j;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        uint32_t x = bm[j][t];
-        while (x) {
-          const uint32_t s = 32 * t + __ffs(x) - 1;
-          x &= x - 1;
-          E[d++] = s * 128 + bk;
-        }
-      }
-    }
-    __syncwarp();
-    if (a.probe == 3) continue;
-
-    // ---- values: E[i] = (~code << 16) | pos, ascending = output order ----
-    for (uint32_t i0 = 0; i0 < H; i0 += 128) {
-      uint32_t pos[4], val[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t i = i0 + 32 * u + lane;
-        pos[u] = i < H ? E[i] : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) val[u] = __ldg(xr + pos[u]);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t i = i0 + 32 * u + lane;
-        if (i < H) E[i] = ((~asc_code16(val[u]) & 0xffffu) << 16) | pos[u];
-      }
-    }
-    __syncwarp();
-    if (a.probe == 4) continue;
-
-    // ---- crowded buckets: Alg. 1 over the bucket's hits in position order;
-    //      the K' survivors stay at the front of the segment
-    uint32_t dropped = 0;
-    for (uint32_t i = lane; i < nov; i += 32) {
-      const uint32_t ds = tmp[i], off = ds & 0xffffu, cb = ds >> 16;
-      uint32_t s0 = kRgDead, s1 = kRgDead, s2 = kRgDead, s3 = kRgDead;
-      for (uint32_t q = 0; q < cb; ++q) {
-        const uint32_t e = E[off + q];
-        if ((e >> 16) <= (s3 >> 16)) {  // value >= v[K' - 1]: replace the minimum slot
-          s3 = e;
-          if ((s3 >> 16) < (s2 >> 16)) { const uint32_t z = s3; s3 = s2; s2 = z; }
-          if ((s2 >> 16) < (s1 >> 16)) { const uint32_t z = s2; s2 = s1; s1 = z; }
-          if ((s1 >> 16) < (s0 >> 16)) { const uint32_t z = s1; s1 = s0; s0 = z; }
-        }
-      }
-      E[off] = s0;
-      E[off + 1] = s1;
-      E[off + 2] = s2;
-      E[off + 3] = s3;
-      for (uint32_t q = 4; q < cb; ++q) E[off + q] = kRgDead;
-      dropped += cb - 4;
-    }
-    dropped = __reduce_add_sync(0xffffffffu, dropped);
-    const uint32_t M = H - dropped;
-    __syncwarp();
-    if (a.probe == 5) continue;
-
-    // ---- stage 2: the first K of the M >= K candidates -------------------
-    if (binned) {
-      auto bin_of = [&](uint32_t key) {
-        return ((kmax - (~(key >> 16) & 0xffffu)) << 2) | ((key & 0xffffu) >> a.sub_shift);
-      };
-      for (uint32_t x = lane; x < H; x += 32) {
-        const uint32_t key = E[x];
-        if (key != kRgDead) atomicAdd(&bins[bin_of(key)], 1u);
+      for (int r = 0; r < 16; ++r) {
+        keys[r] = cand[32 * r + lane];
+        if (keys[r]) atomicAdd(&bins[bin_of(keys[r])], 1u);
       }
       __syncwarp();
       // exclusive scan of the 1024 bins (32 per lane), the first bin starting at >= K
@@ -454,12 +408,14 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
       }
       blim = __reduce_min_sync(0xffffffffu, blim);
       lim = min(M, __reduce_min_sync(0xffffffffu, lim));
+      // bin blim - 1 is not empty and starts below K: it holds the K-th candidate
+      if (blim != 0xffffffffu && blim > 0) Lstar = (kmaxm - ((blim - 1) >> 2)) | (posmode ? 0x8000u : 0u);
       __syncwarp();
-      for (uint32_t x = lane; x < H; x += 32) {  // scatter the bins wholly below rank K
-        const uint32_t key = E[x];
-        if (key != kRgDead) {
-          const uint32_t bn = bin_of(key);
-          if (bn < blim) tmp[atomicAdd(&bins[bn], 1u)] = key;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {  // scatter the bins wholly below rank K
+        if (keys[r]) {
+          const uint32_t bn = bin_of(keys[r]);
+          if (bn < blim) tmp[atomicAdd(&bins[bn], 1u)] = keys[r];
         }
       }
       __syncwarp();  // bins[b] = end of bin b = start of bin b + 1
@@ -467,25 +423,39 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
         const uint32_t key = tmp[x], bn = bin_of(key);
         const uint32_t b0 = bn ? bins[bn - 1] : 0u, b1 = bins[bn];
         uint32_t r = b0;
-        for (uint32_t y = b0; y < b1; ++y) r += tmp[y] < key ? 1u : 0u;
+        for (uint32_t y = b0; y < b1; ++y) r += tmp[y] < key ? 1u : 0u;  // same code: by position
         if (r < K) {
-          ov[r] = __uint_as_float(code16_bits(~(key >> 16) & 0xffffu) << 16);
+          const uint32_t code = key >> 16;
+          ov[r] = __uint_as_float((posmode ? code : code16_bits(code)) << 16);
           oi[r] = key & 0xffffu;
         }
       }
-    } else {  // the hits span more than 256 value codes: sort them
-      uint32_t P2 = 2;
-      while (P2 < H) P2 <<= 1;
-      for (uint32_t x = H + lane; x < P2; x += 32) E[x] = kRgDead;
-      __syncwarp();
-      warp_bitonic_sort<uint32_t>(E, P2, lane);
-      for (uint32_t x = lane; x < K; x += 32) {
-        ov[x] = __uint_as_float(code16_bits(~(E[x] >> 16) & 0xffffu) << 16);
-        oi[x] = E[x] & 0xffffu;
+    } else {  // the hits span more than 256 value codes: sort the candidates
+      uint32_t off = 0;
+      for (uint32_t r = 0; r < 16; ++r) {
+        const uint32_t e = cand[32 * r + lane];
+        const uint32_t bal = __ballot_sync(0xffffffffu, e != 0);
+        const uint32_t asc = (e >> 16) | (posmode ? 0x8000u : 0u);
+        if (e) tmp[off + __popc(bal & lt)] = ((~asc & 0xffffu) << 16) | (e & 0xffffu);
+        off += __popc(bal);
       }
+      uint32_t P2 = 2;
+      while (P2 < off) P2 <<= 1;
+      for (uint32_t x = off + lane; x < P2; x += 32) tmp[x] = 0xffffffffu;
+      __syncwarp();
+      warp_bitonic_sort<uint32_t>(tmp, P2, lane);
+      for (uint32_t x = lane; x < K; x += 32) {
+        ov[x] = __uint_as_float(code16_bits(~(tmp[x] >> 16) & 0xffffu) << 16);
+        oi[x] = tmp[x] & 0xffffu;
+      }
+      Lstar = ~(tmp[K - 1] >> 16) & 0xffffu;
     }
+    // the next row's prediction
+    if (lane == 0) pred = max(Lstar, kRgKeyNegInf + 1 + a.margin) - a.margin;
     __syncwarp();
   }
+  // a starter that found no prediction must still release the waiting warps
+  if (pred == 0) pred = 0xffffffffu;
 }
 
 }  // namespace atkg

@@ -109,12 +109,13 @@ def test_rowreg_forced_paths(cuda, ref, opts, force):
     check(ref, cuda, x, 287)
 
 
-@pytest.mark.parametrize("margin,slack", [(0, 0), (0, 200), (40, 30), (6, 2)])
-def test_rowreg_prediction_settings(cuda, ref, opts, margin, slack):
-    """The prediction only steers speed: any margin / controller band is exact."""
+@pytest.mark.parametrize("margin,starters", [(0, 4), (1, 1), (40, 4), (5, 16), (5, 64), (300, 2)])
+def test_rowreg_prediction_settings(cuda, ref, opts, margin, starters):
+    """The prediction only steers speed: any margin below the last row's
+    level, and any number of warps starting without one, is exact."""
     opts("rowreg_margin", margin)
-    opts("rowreg_slack", slack)
-    x = np.random.default_rng(margin + slack).standard_normal((2000, 14336)).astype(np.float32)
+    opts("rowreg_starters", starters)
+    x = np.random.default_rng(margin + starters).standard_normal((2000, 14336)).astype(np.float32)
     check(ref, cuda, x, 287)
 
 

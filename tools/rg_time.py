@@ -44,15 +44,15 @@ def main():
         with opt("rowreg_warps", w):
             line(f"rowreg warps={w}", timeit(run))
             if "--probe" in sys.argv:
-                for pr, what in [(1, "stream"), (2, "+ check/bisect"), (3, "+ list"), (4, "+ values"), (5, "+ crowded")]:
+                for pr, what in [(1, "pass"), (2, "+ check/bisect")]:
                     with opt("rowreg_probe", pr):
                         line(f"  warps={w} probe {pr} ({what})", timeit(run))
             with opt("rowreg_force", 1):
                 line(f"  warps={w} every row two-pass", timeit(run))
     if "--sweep" in sys.argv:
-        for m, s in [(2, 30), (6, 10), (6, 60), (12, 30), (3, 20)]:
-            with opt("rowreg_margin", m), opt("rowreg_slack", s):
-                line(f"margin={m} slack={s}", timeit(run))
+        for m, s in [(2, 4), (3, 4), (5, 4), (8, 4), (5, 1), (5, 2), (5, 8), (5, 16)]:
+            with opt("rowreg_margin", m), opt("rowreg_starters", s):
+                line(f"margin={m} starters={s}", timeit(run))
     with opt("rowreg", 0):
         line("row_resident_kernel (previous default)", timeit(run, iters=20))
     atk.check_status(st)
