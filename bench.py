@@ -325,6 +325,8 @@ class RowsWorkload:
         # threshold stream, short bf16 rows the row-resident kernels
         if self.n >= 32768:
             return "st_stream_kernel (threshold stream; stage-1 pass)"
+        if self.esz == 2 and self.b == 128 and self.kp == 4 and self.n in (3584, 7168, 14336, 16384):
+            return "row_reg_kernel (one warp per row, streamed once; stage 1 + stage 2)"
         if self.n * self.esz <= 64 * 1024:
             return "row_threshold_kernel" if self.kp >= 8 else "row_resident_kernel"
         return "stage1_flat_kernel"

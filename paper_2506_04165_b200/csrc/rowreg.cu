@@ -11,9 +11,9 @@ namespace atkg {
 
 namespace {
 
-template <int S, int NW>
+template <int S, int NW, int PF>
 void rg_launch(const RgPlan& rp, const RgArgs& a, cudaStream_t st) {
-  auto kern = row_reg_kernel<S, NW>;
+  auto kern = row_reg_kernel<S, NW, PF>;
   ensure_smem_fn(kern, rp.smem);
   kern<<<rp.grid, 32 * NW, rp.smem, st>>>(a);
   check_launch();
@@ -22,11 +22,14 @@ void rg_launch(const RgPlan& rp, const RgArgs& a, cudaStream_t st) {
 template <int S>
 void rg_dispatch(const RgPlan& rp, const RgArgs& a, cudaStream_t st) {
   switch (rp.warps) {
-    case 8: rg_launch<S, 8>(rp, a, st); break;
-    case 12: rg_launch<S, 12>(rp, a, st); break;
-    case 16: rg_launch<S, 16>(rp, a, st); break;
-    case 20: rg_launch<S, 20>(rp, a, st); break;
-    default: rg_launch<S, 22>(rp, a, st); break;
+    case 12: rg_launch<S, 12, 1>(rp, a, st); break;
+    case 16: rg_launch<S, 16, 1>(rp, a, st); break;
+    case 20: rg_launch<S, 20, 1>(rp, a, st); break;
+    case 24: rg_launch<S, 24, 1>(rp, a, st); break;
+    case 28: rg_launch<S, 28, 0>(rp, a, st); break;
+    case 29: rg_launch<S, 28, 1>(rp, a, st); break;
+    case 32: rg_launch<S, 32, 0>(rp, a, st); break;
+    default: rg_launch<S, 32, 1>(rp, a, st); break;
   }
 }
 
@@ -43,9 +46,10 @@ RgPlan plan_rowreg(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_
   if (k > kRgTmp || (uint64_t)k > B * kp) return rp;
   if (reinterpret_cast<uintptr_t>(in) % 8 != 0) return rp;
   rp.S = (uint32_t)S;
-  uint32_t w = (uint32_t)opt("rowreg_warps", 20);
-  rp.warps = w <= 8 ? 8 : w <= 12 ? 12 : w <= 16 ? 16 : w <= 20 ? 20 : 22;
-  rp.smem = (size_t)rp.warps * kRgWarpSmem;
+  // warps per CTA (= per SM); 29 / 33 = 28 / 32 warps with the loads issued one tile ahead
+  uint32_t w = (uint32_t)opt("rowreg_warps", 29);
+  rp.warps = w <= 12 ? 12 : w <= 16 ? 16 : w <= 20 ? 20 : w <= 24 ? 24 : w <= 28 ? 28 : w == 29 ? 29 : w <= 32 ? 32 : 33;
+  rp.smem = (size_t)std::min<uint32_t>(rp.warps, 32) * kRgWarpSmem;
   rp.sub_shift = 0;
   while ((n - 1) >> rp.sub_shift >= 4) ++rp.sub_shift;
   rp.grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(rows, (uint64_t)sm_count()));
@@ -61,7 +65,6 @@ void run_rowreg(const RgPlan& rp, const void* in, uint64_t rows, uint32_t k, flo
   a.k = k;
   a.sub_shift = rp.sub_shift;
   a.margin = (uint32_t)opt("rowreg_margin", 5);
-  a.starters = (uint32_t)std::max<uint64_t>(1, opt("rowreg_starters", 4));
   a.force = (uint32_t)opt("rowreg_force", 0);
   a.probe = (uint32_t)opt("rowreg_probe", 0);
   a.out_v = ov;

@@ -32,10 +32,9 @@
 //               bucket holding the large values): Alg. 1 of every bucket as
 //               the reference runs it, then a bitonic sort of the B K' rank
 //               keys.  Slow; degenerate rows only.
-// After the pass: crowded buckets (c_b > K') are resolved by Alg. 1 over
-// their logged hits (one lane per crowded bucket), then the (value code,
-// index quarter) counting sort of rowwarp.cuh writes the first K in output
-// order (topk.cpp:30-50).
+// After the pass the states hold the row's candidates >= L; a bitonic sort
+// of the 512 slots in registers writes the first K in output order
+// (topk.cpp:30-50).
 #pragma once
 
 #include <cuda_bf16.h>
@@ -45,12 +44,12 @@
 
 namespace atkg {
 
-constexpr uint32_t kRgBins = 1024;           // 256 value codes x 4 index quarters
 constexpr uint32_t kRgTmp = 512;             // candidates: <= B K'
 constexpr uint32_t kRgKeyNegInf = 0x007fu;   // asc_code16(-inf)
 constexpr int kRgTile = 8;                   // stride-rows per load batch = per staging tile
-// per warp: staging tile [8][32] x 8 B | state [128 buckets][4] u32 | bins | tmp
-constexpr uint32_t kRgWarpSmem = kRgTile * 256 + 4 * 512 + 4 * kRgBins + 4 * kRgTmp;
+// per warp: staging tile [8][32] x 8 B (the sorted keys after the pass) | state [128 buckets][4] u32
+constexpr uint32_t kRgWarpSmem = kRgTile * 256 + 4 * 512;
+static_assert(kRgTile * 256 == 4 * kRgTmp, "tmp reuses the staging tile");
 
 struct RgArgs {
   const uint16_t* in;
@@ -58,8 +57,7 @@ struct RgArgs {
   uint32_t k;
   uint32_t sub_shift;   // pos >> sub_shift < 4
   uint32_t margin;      // prediction: codes below the level of the last row's K-th candidate
-  uint32_t starters;    // warps per CTA that start without a prediction (the rest wait for one)
-  uint32_t force;       // tests: 1 = every row two-pass, 2 = every row exact, 3 = sort instead of bins
+  uint32_t force;       // tests: 1 = every row two-pass, 2 = every row exact
   uint32_t probe;       // development: stop after phase `probe`
   float* out_v;
   uint32_t* out_i;
@@ -128,23 +126,25 @@ __host__ __device__ constexpr int rg_group(int s) {
 // (value descending, a later equal element never passes an earlier one; the
 // empty slots are 0, below every hit).  POS: the hits are strictly positive,
 // their bf16 bits order as they are; otherwise ascending codes.
-template <int S, bool MAX, bool POS>
+template <int S, bool MAX, bool POS, int PF>
 __device__ __forceinline__ void rg_stream(const uint2* p, uint32_t L2, uint32_t lane, uint2* stage, uint4* state,
                                           uint32_t (&gm)[2][4]) {
   constexpr int NB = (S + kRgTile - 1) / kRgTile;
-  uint2 buf[2][kRgTile];
+  uint2 buf[PF + 1][kRgTile];
+  if (PF) {
 #pragma unroll
-  for (int i = 0; i < kRgTile; ++i)
-    if (i < S) buf[0][i] = rg_ldg(p + i * 32);
+    for (int i = 0; i < kRgTile; ++i)
+      if (i < S) buf[0][i] = rg_ldg(p + i * 32);
+  }
   const uint8_t* col = reinterpret_cast<const uint8_t*>(stage + lane);
   uint4* st4 = state + 4 * lane;  // the lane's buckets 4 lane .. 4 lane + 3
 #pragma unroll
   for (int bt = 0; bt < NB; ++bt) {
-    if (bt + 1 < NB) {
+    if (bt + PF < NB) {
 #pragma unroll
       for (int i = 0; i < kRgTile; ++i) {
-        const int s = (bt + 1) * kRgTile + i;
-        if (s < S) buf[(bt + 1) & 1][i] = rg_ldg(p + s * 32);
+        const int s = (bt + PF) * kRgTile + i;
+        if (s < S) buf[(bt + PF) % (PF + 1)][i] = rg_ldg(p + s * 32);
       }
     }
     uint32_t m = 0;
@@ -152,7 +152,7 @@ __device__ __forceinline__ void rg_stream(const uint2* p, uint32_t L2, uint32_t 
     for (int i = 0; i < kRgTile; ++i) {
       const int s = bt * kRgTile + i;
       if (s < S) {
-        const uint2 v = buf[bt & 1][i];
+        const uint2 v = buf[bt % (PF + 1)][i];
         if (MAX) {
           const int g = rg_group<S>(s);
           gm[0][g] = bmax_nan(gm[0][g], v.x);
@@ -164,10 +164,11 @@ __device__ __forceinline__ void rg_stream(const uint2* p, uint32_t L2, uint32_t 
       }
     }
     while (m) {
-      const uint32_t b = 31u - (uint32_t)__clz((int)m);
+      uint32_t b;
+      asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(m));
       m ^= 1u << b;
-      const uint32_t r = b & 7u, u = b >> 3;           // stride-row bt * 8 + 7 - r, element slot u
-      const uint32_t j = ((u & 1u) << 1) | (u >> 1);    // bucket 4 lane + j
+      const uint32_t r = b & 7u;                         // stride-row bt * 8 + 7 - r
+      const uint32_t j = ((b >> 2) & 2u) | (b >> 4);     // element slot b >> 3 -> bucket 4 lane + j
       uint32_t val = *reinterpret_cast<const uint16_t*>(col + r * 256 + j * 2);
       if (!POS) val = asc_code16(val);
       const uint32_t e = (val << 16) | (((bt * kRgTile + 7) << 7) - (r << 7) + 4 * lane + j);
@@ -241,8 +242,8 @@ __device__ __noinline__ void rg_exact(const uint16_t* xr, uint32_t lane, uint32_
 // S = stride-rows (n = 128 S <= 16384), B = 128, K' = 4.  One CTA per SM;
 // CTA c owns the rows [rows c / G, rows (c + 1) / G) and its warps pull them
 // from a shared counter.  `pred` is the CTA's prediction (an ascending code;
-// 0 = none yet, ~0 = the starters found none).
-template <int S, int NW>
+// ~0 = none).
+template <int S, int NW, int PF>
 __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
   constexpr uint32_t n = 128u * S;
   extern __shared__ __align__(128) uint8_t rg_smem[];
@@ -253,21 +254,62 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
   uint8_t* wsm = rg_smem + (size_t)wid * kRgWarpSmem;
   uint2* stage = reinterpret_cast<uint2*>(wsm);
   uint4* state = reinterpret_cast<uint4*>(wsm + kRgTile * 256);
-  uint32_t* cand = reinterpret_cast<uint32_t*>(state);  // [bucket][4], 0 = empty
-  uint32_t* bins = cand + 512;
-  uint32_t* tmp = bins + kRgBins;
+  uint32_t* tmp = reinterpret_cast<uint32_t*>(wsm);     // the staging tile is dead after the pass
   const uint64_t r0 = a.rows * blockIdx.x / gridDim.x, r1 = a.rows * (blockIdx.x + 1) / gridDim.x;
   const uint32_t nrows = (uint32_t)(r1 - r0);
   if (threadIdx.x == 0) {
     queue = 0;
-    pred = 0;
+    pred = 0xffffffffu;
+  }
+  // ---- prologue: the first prediction from the CTA's first row.  Every warp
+  // takes a share of its stride-rows (one DRAM round trip for the CTA instead
+  // of a lone warp's latency-bound pass), the group maxima are combined in
+  // shared memory and warp 0 bisects the guaranteed level (K-th largest group
+  // maximum).  A NaN or -inf-heavy first row leaves no prediction.
+  if (a.force == 0) {
+    const uint2* p0 = reinterpret_cast<const uint2*>(a.in + r0 * n) + lane;
+    uint32_t pm[2][4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      pm[0][g] = pm[1][g] = 0xff80ff80u;
+      const int s1 = g == 3 ? S : (g + 1) * S / 4;
+      for (int s = g * S / 4 + (int)wid; s < s1; s += NW) {
+        const uint2 v = rg_ldg(p0 + s * 32);
+        pm[0][g] = bmax_nan(pm[0][g], v.x);
+        pm[1][g] = bmax_nan(pm[1][g], v.y);
+      }
+    }
+    uint32_t* part = reinterpret_cast<uint32_t*>(wsm);  // [8][32] per warp, in its staging tile
+#pragma unroll
+    for (int w = 0; w < 2; ++w)
+#pragma unroll
+      for (int g = 0; g < 4; ++g) part[(4 * w + g) * 32 + lane] = pm[w][g];
+    __syncthreads();
+    if (wid < 8) {  // warp q folds word q of every warp's share
+      uint32_t m = 0xff80ff80u;
+      for (uint32_t w2 = 0; w2 < (uint32_t)NW; ++w2)
+        m = bmax_nan(m, reinterpret_cast<const uint32_t*>(rg_smem + (size_t)w2 * kRgWarpSmem)[wid * 32 + lane]);
+      part[256 + lane] = m;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t gm0[2][4];
+#pragma unroll
+      for (int w = 0; w < 2; ++w)
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+          gm0[w][g] = reinterpret_cast<const uint32_t*>(rg_smem + (size_t)(4 * w + g) * kRgWarpSmem)[256 + lane];
+      uint32_t cur = 0;
+#pragma unroll 1
+      for (int bit = 15; bit >= 0; --bit) {
+        const uint32_t t = cur | (1u << bit);
+        const uint32_t cg = __reduce_add_sync(0xffffffffu, rg_count_ge(gm0, rg_bits2(t)));
+        if (cg >= K) cur = t;
+      }
+      if (cur > kRgKeyNegInf && lane == 0) pred = cur << 4;
+    }
   }
   __syncthreads();
-  const uint32_t lt = (1u << lane) - 1u;
-  // every warp but the starters waits for the first prediction
-  if (wid >= a.starters && a.force == 0) {
-    while (pred == 0) __nanosleep(500);
-  }
 
 #pragma unroll 1
   for (;;) {
@@ -292,14 +334,15 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
       for (int j = 0; j < 4; ++j) state[4 * lane + j] = make_uint4(0, 0, 0, 0);
     };
     clear_state();
-    uint32_t Lkey = pred;
-    const bool have = Lkey != 0 && Lkey != 0xffffffffu && a.force == 0;
+    const uint32_t pr = pred;  // running mean of the rows' K-th candidate levels, x 16
+    const bool have = pr != 0xffffffffu && a.force == 0;
+    uint32_t Lkey = max(pr >> 4, kRgKeyNegInf + 1 + a.margin) - a.margin;
     bool posmode = have && Lkey > 0x8000u;
     if (have) {
-      if (posmode) rg_stream<S, true, true>(p, rg_bits2(Lkey), lane, stage, state, gm);
-      else rg_stream<S, true, false>(p, rg_bits2(Lkey), lane, stage, state, gm);
+      if (posmode) rg_stream<S, true, true, PF>(p, rg_bits2(Lkey), lane, stage, state, gm);
+      else rg_stream<S, true, false, PF>(p, rg_bits2(Lkey), lane, stage, state, gm);
     } else {
-      rg_stream<S, true, true>(p, 0x7fc07fc0u, lane, stage, state, gm);  // NaN level: maxima only
+      rg_stream<S, true, true, PF>(p, 0x7fc07fc0u, lane, stage, state, gm);  // NaN level: maxima only
     }
     if (a.probe == 1) {  // development: the pass alone (its results consumed)
       uint32_t z = state[4 * lane].x;
@@ -308,7 +351,6 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
 #pragma unroll
         for (int g = 0; g < 4; ++g) z += gm[w][g];
       if (z == 0x12345u) oi[lane] = z;
-      if (pred == 0) pred = 0xbff0u;
       continue;
     }
 
@@ -319,10 +361,8 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
     const uint32_t nan = ((mlo & 0x7fffu) > 0x7f80u || (mhi & 0x7fffu) > 0x7f80u) ? 1u : 0u;
     if (__reduce_or_sync(0xffffffffu, nan)) {
       if (lane == 0) atomicOr(a.status, ATKG_FLAG_NAN);
-      if (pred == 0) pred = 0xffffffffu;
       continue;
     }
-    const uint32_t kmax = __reduce_max_sync(0xffffffffu, max(asc_code16(mlo), asc_code16(mhi)));
 
     // M = sum_b min(K', c_b) = the filled slots
     auto filled = [&]() {
@@ -336,7 +376,8 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
     };
     uint32_t M = have ? filled() : 0u;
     bool exact = a.force == 2;
-    if (M < K) {
+    const bool twopass = M < K;
+    if (twopass) {
       // ---- two-pass: the exact K-th largest group maximum guarantees M >= K
       uint32_t cur = 0;
 #pragma unroll 1
@@ -349,113 +390,102 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
       if (Lkey <= kRgKeyNegInf) {
         exact = true;
       } else {
-        if (pred == 0) pred = max(Lkey, kRgKeyNegInf + 1 + a.margin) - a.margin;
         posmode = Lkey > 0x8000u;
         clear_state();
-        if (posmode) rg_stream<S, false, true>(p, rg_bits2(Lkey), lane, stage, state, gm);
-        else rg_stream<S, false, false>(p, rg_bits2(Lkey), lane, stage, state, gm);
+        if (posmode) rg_stream<S, false, true, PF>(p, rg_bits2(Lkey), lane, stage, state, gm);
+        else rg_stream<S, false, false, PF>(p, rg_bits2(Lkey), lane, stage, state, gm);
         M = filled();
       }
     }
     if (a.probe == 2) continue;
     if (exact) {
-      if (pred == 0) pred = 0xffffffffu;
       __syncwarp();
-      rg_exact<S>(xr, lane, K, reinterpret_cast<uint64_t*>(bins), ov, oi);
+      rg_exact<S>(xr, lane, K, reinterpret_cast<uint64_t*>(wsm), ov, oi);  // tile | state: 4 KB
       continue;
     }
     __syncwarp();
 
     // ---- stage 2: the first K of the M >= K candidates -------------------
-    const uint32_t kmaxm = posmode ? (kmax & 0x7fffu) : kmax;
-    const uint32_t Lm = posmode ? (Lkey & 0x7fffu) : Lkey;
-    const bool binned = kmaxm - Lm < 256u && a.force != 3;
-    uint32_t Lstar = Lkey;  // level of the K-th candidate (ascending code)
-    if (binned) {
+    // A bitonic sort of the 512 slots in registers (16 per lane: the lane's
+    // own 4 buckets, each already in Alg. 1 order = ascending key).  Key =
+    // (~code << 16) | position: ascending = output order (value descending,
+    // index ascending, topk.cpp:30-39); an empty slot sorts last.
+    uint32_t Lstar;
+    {
+      uint32_t k[16];
 #pragma unroll
-      for (int i = 0; i < (int)(kRgBins / 128); ++i)
-        reinterpret_cast<uint4*>(bins)[lane + 32 * i] = make_uint4(0, 0, 0, 0);
-      __syncwarp();
-      auto bin_of = [&](uint32_t key) { return ((kmaxm - (key >> 16)) << 2) | ((key & 0xffffu) >> a.sub_shift); };
-      uint32_t keys[16];
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        keys[r] = cand[32 * r + lane];
-        if (keys[r]) atomicAdd(&bins[bin_of(keys[r])], 1u);
+      for (int j = 0; j < 4; ++j) {
+        const uint4 sv = state[4 * lane + j];
+        k[4 * j] = sv.x ^ 0xffff0000u;
+        k[4 * j + 1] = sv.y ^ 0xffff0000u;
+        k[4 * j + 2] = sv.z ^ 0xffff0000u;
+        k[4 * j + 3] = sv.w ^ 0xffff0000u;
       }
-      __syncwarp();
-      // exclusive scan of the 1024 bins (32 per lane), the first bin starting at >= K
-      uint4 cc[8];
-      uint32_t sum = 0;
+      // every merge ascending: its first step pairs g with g ^ (size - 1) (two ascending runs
+      // head to tail), the others g with g ^ dist; element g = 16 lane + i
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        cc[i] = reinterpret_cast<const uint4*>(bins)[8 * lane + i];
-        sum += cc[i].x + cc[i].y + cc[i].z + cc[i].w;
-      }
-      uint32_t tot, st = rg_excl_scan(sum, lane, &tot), blim = 0xffffffffu, lim = 0xffffffffu;
+      for (int size = 8; size <= 512; size <<= 1) {
+        if (size <= 16) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t q0 = st, q1 = q0 + cc[i].x, q2 = q1 + cc[i].y, q3 = q2 + cc[i].z;
-        st = q3 + cc[i].w;
-        reinterpret_cast<uint4*>(bins)[8 * lane + i] = make_uint4(q0, q1, q2, q3);
-        const uint32_t b0 = 32 * lane + 4 * i;
-        if (blim == 0xffffffffu) {
-          if (q0 >= K) { blim = b0; lim = q0; }
-          else if (q1 >= K) { blim = b0 + 1; lim = q1; }
-          else if (q2 >= K) { blim = b0 + 2; lim = q2; }
-          else if (q3 >= K) { blim = b0 + 3; lim = q3; }
+          for (int i = 0; i < 16; ++i) {
+            const int q = i ^ (size - 1);
+            if (i < q) { const uint32_t x = k[i], y = k[q]; k[i] = min(x, y); k[q] = max(x, y); }
+          }
+        } else {
+          const uint32_t lm = (uint32_t)(size >> 4) - 1u;
+          const bool lower = (lane & (uint32_t)(size >> 5)) == 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t ya = __shfl_xor_sync(0xffffffffu, k[15 - i], lm);  // partner's 15 - i -> my i
+            const uint32_t yb = __shfl_xor_sync(0xffffffffu, k[i], lm);       // partner's i -> my 15 - i
+            k[i] = lower ? min(k[i], ya) : max(k[i], ya);
+            k[15 - i] = lower ? min(k[15 - i], yb) : max(k[15 - i], yb);
+          }
+        }
+#pragma unroll
+        for (int dist = size >> 2; dist > 0; dist >>= 1) {
+          if (dist >= 16) {
+            const uint32_t ld = (uint32_t)dist >> 4;
+            const bool lower = (lane & ld) == 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const uint32_t y = __shfl_xor_sync(0xffffffffu, k[i], ld);
+              k[i] = lower ? min(k[i], y) : max(k[i], y);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if ((i & dist) == 0) { const uint32_t x = k[i], y = k[i | dist]; k[i] = min(x, y); k[i | dist] = max(x, y); }
+            }
+          }
         }
       }
-      blim = __reduce_min_sync(0xffffffffu, blim);
-      lim = min(M, __reduce_min_sync(0xffffffffu, lim));
-      // bin blim - 1 is not empty and starts below K: it holds the K-th candidate
-      if (blim != 0xffffffffu && blim > 0) Lstar = (kmaxm - ((blim - 1) >> 2)) | (posmode ? 0x8000u : 0u);
       __syncwarp();
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {  // scatter the bins wholly below rank K
-        if (keys[r]) {
-          const uint32_t bn = bin_of(keys[r]);
-          if (bn < blim) tmp[atomicAdd(&bins[bn], 1u)] = keys[r];
-        }
-      }
-      __syncwarp();  // bins[b] = end of bin b = start of bin b + 1
-      for (uint32_t x = lane; x < lim; x += 32) {
-        const uint32_t key = tmp[x], bn = bin_of(key);
-        const uint32_t b0 = bn ? bins[bn - 1] : 0u, b1 = bins[bn];
-        uint32_t r = b0;
-        for (uint32_t y = b0; y < b1; ++y) r += tmp[y] < key ? 1u : 0u;  // same code: by position
-        if (r < K) {
-          const uint32_t code = key >> 16;
-          ov[r] = __uint_as_float((posmode ? code : code16_bits(code)) << 16);
-          oi[r] = key & 0xffffu;
-        }
-      }
-    } else {  // the hits span more than 256 value codes: sort the candidates
-      uint32_t off = 0;
-      for (uint32_t r = 0; r < 16; ++r) {
-        const uint32_t e = cand[32 * r + lane];
-        const uint32_t bal = __ballot_sync(0xffffffffu, e != 0);
-        const uint32_t asc = (e >> 16) | (posmode ? 0x8000u : 0u);
-        if (e) tmp[off + __popc(bal & lt)] = ((~asc & 0xffffu) << 16) | (e & 0xffffu);
-        off += __popc(bal);
-      }
-      uint32_t P2 = 2;
-      while (P2 < off) P2 <<= 1;
-      for (uint32_t x = off + lane; x < P2; x += 32) tmp[x] = 0xffffffffu;
+      for (int i = 0; i < 16; ++i) tmp[16 * lane + i] = k[i];
       __syncwarp();
-      warp_bitonic_sort<uint32_t>(tmp, P2, lane);
-      for (uint32_t x = lane; x < K; x += 32) {
-        ov[x] = __uint_as_float(code16_bits(~(tmp[x] >> 16) & 0xffffu) << 16);
-        oi[x] = tmp[x] & 0xffffu;
+      if (a.probe == 9) {  // development: path statistics instead of results (out_i[0..1] zeroed by the caller)
+        if (lane == 0) {
+          atomicAdd(a.out_i, twopass ? 1u : 0u);
+          atomicAdd(a.out_i + 1, M);
+        }
+      } else {
+        for (uint32_t x = lane; x < K; x += 32) {
+          const uint32_t key = tmp[x], code = ~(key >> 16) & 0xffffu;
+          ov[x] = __uint_as_float((posmode ? code : code16_bits(code)) << 16);
+          oi[x] = key & 0xffffu;
+        }
       }
-      Lstar = ~(tmp[K - 1] >> 16) & 0xffffu;
+      const uint32_t ck = ~(tmp[K - 1] >> 16) & 0xffffu;  // the K-th candidate's level
+      Lstar = posmode ? (ck | 0x8000u) : ck;
     }
-    // the next row's prediction
-    if (lane == 0) pred = max(Lstar, kRgKeyNegInf + 1 + a.margin) - a.margin;
+    // the next rows' prediction (a racing update by another warp is as good)
+    if (lane == 0) {
+      const uint32_t pv = pred;
+      pred = pv == 0xffffffffu ? Lstar << 4 : (uint32_t)((int)pv + (((int)(Lstar << 4) - (int)pv) >> 2));
+    }
     __syncwarp();
   }
-  // a starter that found no prediction must still release the waiting warps
-  if (pred == 0) pred = 0xffffffffu;
 }
 
 }  // namespace atkg

@@ -84,7 +84,7 @@ def adversarial(n, k, seed):
 
 
 @pytest.mark.parametrize("n,k", SHAPES)
-@pytest.mark.parametrize("warps", [8, 20])
+@pytest.mark.parametrize("warps", [12, 24, 33])
 def test_rowreg_adversarial_vs_reference(cuda, ref, opts, n, k, warps):
     opts("rowreg_warps", warps)
     x = adversarial(n, k, n + k)
@@ -99,7 +99,7 @@ def test_rowreg_ties_vs_reference(cuda, ref, levels):
     check(ref, cuda, x, 287)
 
 
-@pytest.mark.parametrize("force", [1, 2, 3])
+@pytest.mark.parametrize("force", [1, 2])
 def test_rowreg_forced_paths(cuda, ref, opts, force):
     """1 = every row two-pass, 2 = every row on the exact path, 3 = sorted instead of binned."""
     opts("rowreg_force", force)
@@ -109,13 +109,11 @@ def test_rowreg_forced_paths(cuda, ref, opts, force):
     check(ref, cuda, x, 287)
 
 
-@pytest.mark.parametrize("margin,starters", [(0, 4), (1, 1), (40, 4), (5, 16), (5, 64), (300, 2)])
-def test_rowreg_prediction_settings(cuda, ref, opts, margin, starters):
-    """The prediction only steers speed: any margin below the last row's
-    level, and any number of warps starting without one, is exact."""
+@pytest.mark.parametrize("margin", [0, 1, 5, 40, 300])
+def test_rowreg_prediction_settings(cuda, ref, opts, margin):
+    """The prediction only steers speed: any margin below the last row's level is exact."""
     opts("rowreg_margin", margin)
-    opts("rowreg_starters", starters)
-    x = np.random.default_rng(margin + starters).standard_normal((2000, 14336)).astype(np.float32)
+    x = np.random.default_rng(margin).standard_normal((2000, 14336)).astype(np.float32)
     check(ref, cuda, x, 287)
 
 
@@ -140,7 +138,7 @@ def test_rowreg_nan_raises(cuda):
 
 
 @pytest.mark.parametrize("rows", [1, 5, 147, 148, 149, 3000])
-@pytest.mark.parametrize("warps", [12, 16, 22])
+@pytest.mark.parametrize("warps", [16, 28, 29, 32])
 def test_rowreg_row_counts(cuda, ref, opts, rows, warps):
     """One CTA per SM over a contiguous share of the rows: fewer rows than
     CTAs, one row each, ragged shares."""

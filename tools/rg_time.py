@@ -49,10 +49,18 @@ def main():
                         line(f"  warps={w} probe {pr} ({what})", timeit(run))
             with opt("rowreg_force", 1):
                 line(f"  warps={w} every row two-pass", timeit(run))
+    if "--stats" in sys.argv:
+        for m in [1, 2, 3, 5, 8, 12]:
+            with opt("rowreg_margin", m), opt("rowreg_probe", 9):
+                out[1].zero_()
+                run()
+                torch.cuda.synchronize()
+                tp, msum = out[1].view(-1)[:2].tolist()
+                print(f"margin={m}: two-pass rows {tp} of {rows}, mean M {msum / rows:.1f}", flush=True)
     if "--sweep" in sys.argv:
-        for m, s in [(2, 4), (3, 4), (5, 4), (8, 4), (5, 1), (5, 2), (5, 8), (5, 16)]:
-            with opt("rowreg_margin", m), opt("rowreg_starters", s):
-                line(f"margin={m} starters={s}", timeit(run))
+        for m in [1, 2, 3, 4, 5, 6, 8, 12]:
+            with opt("rowreg_margin", m):
+                line(f"margin={m}", timeit(run))
     with opt("rowreg", 0):
         line("row_resident_kernel (previous default)", timeit(run, iters=20))
     atk.check_status(st)
