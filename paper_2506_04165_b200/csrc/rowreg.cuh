@@ -46,10 +46,11 @@ namespace atkg {
 
 constexpr uint32_t kRgTmp = 512;             // candidates: <= B K'
 constexpr uint32_t kRgKeyNegInf = 0x007fu;   // asc_code16(-inf)
-constexpr int kRgTile = 8;                   // stride-rows per load batch = per staging tile
+constexpr int kRgTile = 7;                   // stride-rows per load batch = per staging tile (7 hit bits per
+                                             // bucket and tile fit a bf16 counter exactly: 128 + bits)
 // per warp: staging tile [8][32] x 8 B (the sorted keys after the pass) | state [128 buckets][4] u32
-constexpr uint32_t kRgWarpSmem = kRgTile * 256 + 4 * 512;
-static_assert(kRgTile * 256 == 4 * kRgTmp, "tmp reuses the staging tile");
+constexpr uint32_t kRgWarpSmem = 8 * 256 + 4 * 512;
+static_assert(8 * 256 == 4 * kRgTmp, "the sorted keys reuse the staging tile");
 
 struct RgArgs {
   const uint16_t* in;
@@ -74,6 +75,19 @@ __device__ __forceinline__ uint32_t rg_ge(uint32_t w, uint32_t L2) {
   uint32_t h;
   asm("set.ge.u32.bf16x2 %0, %1, %2;" : "=r"(h) : "r"(w), "r"(L2));
   return h;
+}
+// 1.0 (bf16) in each half whose bf16 is >= the matching half of L2 or unordered (a NaN element
+// counts as a hit: it reaches stage 2 and is reported there)
+__device__ __forceinline__ uint32_t rg_geu1(uint32_t w, uint32_t L2) {
+  uint32_t h;
+  asm("set.geu.bf16x2.bf16x2 %0, %1, %2;" : "=r"(h) : "r"(w), "r"(L2));
+  return h;
+}
+// packed bf16 a * 2 + b on the FMA pipe (the ALU pipe is this kernel's bottleneck)
+__device__ __forceinline__ uint32_t rg_shl_add(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(0x40004000u), "r"(b));
+  return d;
 }
 __device__ __forceinline__ uint32_t rg_bits2(uint32_t code) {
   const uint32_t b = code16_bits(code);
@@ -115,21 +129,27 @@ __host__ __device__ constexpr int rg_group(int s) {
   return g;
 }
 
-// One pass over the row: lane-local group maxima (MAX) and Alg. 1
-// (topk.cpp:80-102) over the hits of each of the lane's 4 buckets, in stream
-// order.  Per tile of 8 stride-rows: the loads (issued one tile ahead) are
-// compared against L2 and copied to the lane's column of the staging tile;
-// bit 8 u + 7 - i of the tile's hit mask = element slot u of stride-row i
+// The hit pass over the row: Alg. 1 (topk.cpp:80-102) over the hits (>= L2,
+// or NaN) of each of the lane's 4 buckets, in stream order.  Per tile of 7
+// stride-rows: the loads (issued PF tiles ahead) are compared against L2 --
+// one packed compare (ALU pipe) and one packed a * 2 + hit (FMA pipe) per
+// word, so after 7 stride-rows each bf16 half holds 128 + its 7 hit bits
+// exactly -- and copied to the lane's column of the staging tile.  Bit
+// 8 u + 6 - i of the tile's hit mask = element slot u of stride-row i
 // (u = 0, 1, 2, 3 <-> bucket 4 lane + 0, 2, 1, 3); the lane then walks the
 // set bits from the top (ascending stride-row inside a slot) and inserts
 // (code << 16 | position) into the bucket's state[4], kept in Alg. 1 order
 // (value descending, a later equal element never passes an earlier one; the
 // empty slots are 0, below every hit).  POS: the hits are strictly positive,
-// their bf16 bits order as they are; otherwise ascending codes.
-template <int S, bool MAX, bool POS, int PF>
-__device__ __forceinline__ void rg_stream(const uint2* p, uint32_t L2, uint32_t lane, uint2* stage, uint4* state,
-                                          uint32_t (&gm)[2][4]) {
+// their bf16 bits order as they are (a NaN sorts first); otherwise ascending
+// codes, and a NaN raises `nan`.
+template <int S, bool POS, int PF>
+__device__ __forceinline__ void rg_hits(const uint2* p, const uint8_t* nxt, uint32_t L2, uint32_t lane, uint2* stage,
+                                        uint4* state, uint32_t& nan) {
   constexpr int NB = (S + kRgTile - 1) / kRgTile;
+  constexpr int AH = 3;                    // L2 prefetch distance in tiles (7 x 256 B = 14 lines each)
+  constexpr uint32_t TB = kRgTile * 256;   // bytes per tile
+  const uint8_t* rowb = reinterpret_cast<const uint8_t*>(p) - 8 * lane;
   uint2 buf[PF + 1][kRgTile];
   if (PF) {
 #pragma unroll
@@ -147,31 +167,40 @@ __device__ __forceinline__ void rg_stream(const uint2* p, uint32_t L2, uint32_t 
         if (s < S) buf[(bt + PF) % (PF + 1)][i] = rg_ldg(p + s * 32);
       }
     }
-    uint32_t m = 0;
+    // pull the tile AH ahead into L2 (of this row, then of the warp's next row): the register
+    // loads one tile ahead then wait on L2, not on DRAM
+    if (lane < TB / 128) {
+      const uint8_t* q = bt + AH < NB ? rowb + (bt + AH) * TB : (nxt ? nxt + (bt + AH - NB) * TB : nullptr);
+      if (q && (bt + AH < NB ? (bt + AH) * TB + lane * 128 < (uint32_t)S * 256 : true))
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(q + lane * 128));
+    }
+    uint32_t ax = 0x3f803f80u, ay = 0x3f803f80u;  // 1.0 | 1.0
 #pragma unroll
     for (int i = 0; i < kRgTile; ++i) {
       const int s = bt * kRgTile + i;
       if (s < S) {
         const uint2 v = buf[bt % (PF + 1)][i];
-        if (MAX) {
-          const int g = rg_group<S>(s);
-          gm[0][g] = bmax_nan(gm[0][g], v.x);
-          gm[1][g] = bmax_nan(gm[1][g], v.y);
-        }
-        m |= rg_ge(v.x, L2) & (0x00010001u << (7 - i));
-        m |= rg_ge(v.y, L2) & (0x01000100u << (7 - i));
-        stage[(7 - i) * 32 + lane] = v;
+        ax = rg_shl_add(ax, rg_geu1(v.x, L2));
+        ay = rg_shl_add(ay, rg_geu1(v.y, L2));
+        stage[(6 - i) * 32 + lane] = v;
+      } else {
+        ax = rg_shl_add(ax, 0u);
+        ay = rg_shl_add(ay, 0u);
       }
     }
+    uint32_t m = (ax & 0x007f007fu) | ((ay & 0x007f007fu) << 8);
     while (m) {
       uint32_t b;
       asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(m));
       m ^= 1u << b;
-      const uint32_t r = b & 7u;                         // stride-row bt * 8 + 7 - r
+      const uint32_t r = b & 7u;                         // stride-row bt * 7 + 6 - r
       const uint32_t j = ((b >> 2) & 2u) | (b >> 4);     // element slot b >> 3 -> bucket 4 lane + j
       uint32_t val = *reinterpret_cast<const uint16_t*>(col + r * 256 + j * 2);
-      if (!POS) val = asc_code16(val);
-      const uint32_t e = (val << 16) | (((bt * kRgTile + 7) << 7) - (r << 7) + 4 * lane + j);
+      if (!POS) {
+        if ((val & 0x7fffu) > 0x7f80u) nan = 1u;
+        val = asc_code16(val);
+      }
+      const uint32_t e = (val << 16) | (((bt * kRgTile + 6) << 7) - (r << 7) + 4 * lane + j);
       uint4 sv = st4[j];
       if (sv.w <= (e | 0xffffu)) {  // value >= v[K' - 1]: e replaces the minimum slot, then rises
         const uint32_t eb = e & 0xffff0000u;  // past the strictly smaller values
@@ -181,6 +210,28 @@ __device__ __forceinline__ void rg_stream(const uint2* p, uint32_t L2, uint32_t 
         sv.y = a1 ? sv.y : (a0 ? e : sv.x);
         sv.x = a0 ? sv.x : e;
         st4[j] = sv;
+      }
+    }
+  }
+}
+
+// The maxima pass (rows without a usable prediction): lane-local maxima of
+// the K' = 4 groups of stride-rows of the lane's buckets, NaN-propagating.
+template <int S>
+__device__ __forceinline__ void rg_max(const uint2* p, uint32_t (&gm)[2][4]) {
+  constexpr int U = 14;
+#pragma unroll
+  for (int s0 = 0; s0 < S; s0 += U) {
+    uint2 v[U];
+#pragma unroll
+    for (int i = 0; i < U; ++i)
+      if (s0 + i < S) v[i] = rg_ldg(p + (s0 + i) * 32);
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      if (s0 + i < S) {
+        const int g = rg_group<S>(s0 + i);
+        gm[0][g] = bmax_nan(gm[0][g], v[i].x);
+        gm[1][g] = bmax_nan(gm[1][g], v[i].y);
       }
     }
   }
@@ -239,12 +290,12 @@ __device__ __noinline__ void rg_exact(const uint16_t* xr, uint32_t lane, uint32_
   __syncwarp();
 }
 
-// S = stride-rows (n = 128 S <= 16384), B = 128, K' = 4.  One CTA per SM;
+// S = stride-rows (n = 128 S <= 16384), B = 128, K' = 4.  CPS CTAs of NW warps per SM;
 // CTA c owns the rows [rows c / G, rows (c + 1) / G) and its warps pull them
 // from a shared counter.  `pred` is the CTA's prediction (an ascending code;
 // ~0 = none).
-template <int S, int NW, int PF>
-__global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
+template <int S, int NW, int PF, int CPS>
+__global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
   constexpr uint32_t n = 128u * S;
   extern __shared__ __align__(128) uint8_t rg_smem[];
   __shared__ uint32_t queue;
@@ -311,59 +362,29 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
   }
   __syncthreads();
 
+  auto pop = [&]() {
+    uint32_t r = 0;
+    if (lane == 0) r = atomicAdd(&queue, 1u);
+    return __shfl_sync(0xffffffffu, r, 0);
+  };
+  uint32_t rnext = pop();
 #pragma unroll 1
   for (;;) {
-    uint32_t rr = 0;
-    if (lane == 0) rr = atomicAdd(&queue, 1u);
-    rr = __shfl_sync(0xffffffffu, rr, 0);
+    const uint32_t rr = rnext;
     if (rr >= nrows) break;
+    rnext = pop();  // one row ahead: its first tiles are prefetched into L2 during this row
+    const uint8_t* nxt = rnext < nrows ? reinterpret_cast<const uint8_t*>(a.in + (r0 + rnext) * n) : nullptr;
     const uint64_t row = r0 + rr;
     const uint16_t* xr = a.in + row * n;
     const uint2* p = reinterpret_cast<const uint2*>(xr) + lane;
     float* ov = a.out_v + row * K;
     uint32_t* oi = a.out_i + row * K;
 
-    // ---- the pass: group maxima + Alg. 1 over the hits against the prediction
-    uint32_t gm[2][4];
-#pragma unroll
-    for (int w = 0; w < 2; ++w)
-#pragma unroll
-      for (int g = 0; g < 4; ++g) gm[w][g] = 0xff80ff80u;
+    // ---- the hit pass against the prediction: Alg. 1 over the hits ---------
     auto clear_state = [&]() {
 #pragma unroll
       for (int j = 0; j < 4; ++j) state[4 * lane + j] = make_uint4(0, 0, 0, 0);
     };
-    clear_state();
-    const uint32_t pr = pred;  // running mean of the rows' K-th candidate levels, x 16
-    const bool have = pr != 0xffffffffu && a.force == 0;
-    uint32_t Lkey = max(pr >> 4, kRgKeyNegInf + 1 + a.margin) - a.margin;
-    bool posmode = have && Lkey > 0x8000u;
-    if (have) {
-      if (posmode) rg_stream<S, true, true, PF>(p, rg_bits2(Lkey), lane, stage, state, gm);
-      else rg_stream<S, true, false, PF>(p, rg_bits2(Lkey), lane, stage, state, gm);
-    } else {
-      rg_stream<S, true, true, PF>(p, 0x7fc07fc0u, lane, stage, state, gm);  // NaN level: maxima only
-    }
-    if (a.probe == 1) {  // development: the pass alone (its results consumed)
-      uint32_t z = state[4 * lane].x;
-#pragma unroll
-      for (int w = 0; w < 2; ++w)
-#pragma unroll
-        for (int g = 0; g < 4; ++g) z += gm[w][g];
-      if (z == 0x12345u) oi[lane] = z;
-      continue;
-    }
-
-    // NaN rows (the reference rejects the input), the row maximum
-    uint32_t mm = bmax_nan(bmax_nan(bmax_nan(gm[0][0], gm[0][1]), bmax_nan(gm[0][2], gm[0][3])),
-                           bmax_nan(bmax_nan(gm[1][0], gm[1][1]), bmax_nan(gm[1][2], gm[1][3])));
-    const uint32_t mlo = mm & 0xffffu, mhi = mm >> 16;
-    const uint32_t nan = ((mlo & 0x7fffu) > 0x7f80u || (mhi & 0x7fffu) > 0x7f80u) ? 1u : 0u;
-    if (__reduce_or_sync(0xffffffffu, nan)) {
-      if (lane == 0) atomicOr(a.status, ATKG_FLAG_NAN);
-      continue;
-    }
-
     // M = sum_b min(K', c_b) = the filled slots
     auto filled = [&]() {
       uint32_t f = 0;
@@ -374,11 +395,39 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
       }
       return __reduce_add_sync(0xffffffffu, f);
     };
-    uint32_t M = have ? filled() : 0u;
+    const uint32_t pr = pred;  // running mean of the rows' K-th candidate levels, x 16
+    const bool have = pr != 0xffffffffu && a.force == 0;
+    uint32_t Lkey = max(pr >> 4, kRgKeyNegInf + 1 + a.margin) - a.margin;
+    bool posmode = Lkey > 0x8000u;
+    uint32_t M = 0, nan = 0;
+    if (have) {
+      clear_state();
+      if (posmode) rg_hits<S, true, PF>(p, nxt, rg_bits2(Lkey), lane, stage, state, nan);
+      else rg_hits<S, false, PF>(p, nxt, rg_bits2(Lkey), lane, stage, state, nan);
+      M = filled();
+    }
+    if (a.probe == 1) {  // development: the pass alone (its results consumed)
+      if (M == 0x12345u) oi[lane] = M;
+      continue;
+    }
     bool exact = a.force == 2;
     const bool twopass = M < K;
     if (twopass) {
-      // ---- two-pass: the exact K-th largest group maximum guarantees M >= K
+      // ---- no usable prediction: the group maxima, the exact K-th largest of
+      //      them (it guarantees M >= K), then the hit pass against it
+      uint32_t gm[2][4];
+#pragma unroll
+      for (int w = 0; w < 2; ++w)
+#pragma unroll
+        for (int g = 0; g < 4; ++g) gm[w][g] = 0xff80ff80u;
+      rg_max<S>(p, gm);
+      const uint32_t mm = bmax_nan(bmax_nan(bmax_nan(gm[0][0], gm[0][1]), bmax_nan(gm[0][2], gm[0][3])),
+                                   bmax_nan(bmax_nan(gm[1][0], gm[1][1]), bmax_nan(gm[1][2], gm[1][3])));
+      nan = ((mm & 0x7fffu) > 0x7f80u || ((mm >> 16) & 0x7fffu) > 0x7f80u) ? 1u : 0u;
+      if (__reduce_or_sync(0xffffffffu, nan)) {  // the reference rejects the input
+        if (lane == 0) atomicOr(a.status, ATKG_FLAG_NAN);
+        continue;
+      }
       uint32_t cur = 0;
 #pragma unroll 1
       for (int bit = 15; bit >= 0; --bit) {
@@ -392,8 +441,8 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
       } else {
         posmode = Lkey > 0x8000u;
         clear_state();
-        if (posmode) rg_stream<S, false, true, PF>(p, rg_bits2(Lkey), lane, stage, state, gm);
-        else rg_stream<S, false, false, PF>(p, rg_bits2(Lkey), lane, stage, state, gm);
+        if (posmode) rg_hits<S, true, PF>(p, nxt, rg_bits2(Lkey), lane, stage, state, nan);
+        else rg_hits<S, false, PF>(p, nxt, rg_bits2(Lkey), lane, stage, state, nan);
         M = filled();
       }
     }
@@ -464,6 +513,12 @@ __global__ void __launch_bounds__(32 * NW, 1) row_reg_kernel(RgArgs a) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) tmp[16 * lane + i] = k[i];
       __syncwarp();
+      // a NaN element was a hit (unordered compare): as raw bits it sorts first
+      if (posmode && ((~(tmp[0] >> 16)) & 0x7fffu) > 0x7f80u) nan = 1u;
+      if (__reduce_or_sync(0xffffffffu, nan)) {  // the reference rejects the input
+        if (lane == 0) atomicOr(a.status, ATKG_FLAG_NAN);
+        continue;
+      }
       if (a.probe == 9) {  // development: path statistics instead of results (out_i[0..1] zeroed by the caller)
         if (lane == 0) {
           atomicAdd(a.out_i, twopass ? 1u : 0u);

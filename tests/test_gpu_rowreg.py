@@ -138,7 +138,7 @@ def test_rowreg_nan_raises(cuda):
 
 
 @pytest.mark.parametrize("rows", [1, 5, 147, 148, 149, 3000])
-@pytest.mark.parametrize("warps", [16, 28, 29, 32])
+@pytest.mark.parametrize("warps", [16, 28, 29, 32, 36, 40])
 def test_rowreg_row_counts(cuda, ref, opts, rows, warps):
     """One CTA per SM over a contiguous share of the rows: fewer rows than
     CTAs, one row each, ragged shares."""
