@@ -813,6 +813,11 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     if (rows == 0) return;
     check_ws(ws_bytes, ws_need(ATKG_OP_APPROX, dtype, rows, *p));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const RgPlan rgp = plan_rowreg(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
+    if (rgp.ok) {  // bf16 rows up to 65536 with B = 128, K' = 4: one warp per row, streamed once into registers (rowreg.cuh)
+      run_rowreg(rgp, d_in, rows, p->global_k, d_out_vals, d_out_idx, d_status, st);
+      return;
+    }
     const StPlan sp = plan_streamthr(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
     if (sp.ok) {  // long rows: threshold stream + per-row finish (exact fallback per row)
       void* sws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(d_ws)));
@@ -835,11 +840,6 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     float* gv = reinterpret_cast<float*>(w);
     uint32_t* gi = reinterpret_cast<uint32_t*>(w + rows * gstride * 4);
     w += grid_bytes(rows, *p);
-    const RgPlan rgp = plan_rowreg(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
-    if (rgp.ok) {  // short bf16 rows streamed once into registers, one warp per row (rowreg.cuh)
-      run_rowreg(rgp, d_in, rows, p->global_k, d_out_vals, d_out_idx, d_status, st);
-      return;
-    }
     // the guaranteed-threshold row kernels (rowwarp.cuh, shortrow.cuh) are
     // bit-exact but not yet faster than row_resident_kernel where that one
     // applies; they run where it does not, or when selected

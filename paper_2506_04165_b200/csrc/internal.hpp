@@ -114,7 +114,7 @@ void run_rowwarp(const RwPlan& rp, const void* in, uint64_t rows, uint64_t n, ui
 // one warp per bf16 row streamed once into registers, B = 128, K' = 4 (rowreg.cu)
 struct RgPlan {
   bool ok = false;
-  uint32_t S = 0, warps = 0, sub_shift = 0, grid = 0;
+  uint32_t S = 0, warps = 0, grid = 0;
   size_t smem = 0;
 };
 RgPlan plan_rowreg(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,

@@ -46,7 +46,7 @@ RgPlan plan_rowreg(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_
   if (!for_size && (!opt("rowreg", 1) || opt("short", 0) || opt("rowwarp", 0))) return rp;
   if (dtype != ATKG_BF16 || B != 128 || kp != 4 || n % 128 != 0) return rp;
   const uint64_t S = n / 128;
-  if (S != 28 && S != 56 && S != 112 && S != 128) return rp;  // instantiated row lengths
+  if (S < 8 || S > 512) return rp;  // positions are 16-bit; K' = 4 groups of >= 2 stride-rows
   if (k > kRgTmp || (uint64_t)k > B * kp) return rp;
   if (reinterpret_cast<uintptr_t>(in) % 8 != 0) return rp;
   rp.S = (uint32_t)S;
@@ -55,8 +55,6 @@ RgPlan plan_rowreg(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_
   rp.warps = w <= 12 ? 12 : w <= 16 ? 16 : w <= 20 ? 20 : w <= 24 ? 24 : w <= 28 ? 28 : w == 29 ? 29 : w <= 32 ? 32 : w == 33 ? 33 : w <= 36 ? 36 : 40;
   const uint32_t cps = rp.warps > 33 ? 2 : 1;
   rp.smem = (size_t)(rp.warps == 29 ? 28 : rp.warps == 33 ? 32 : rp.warps / cps) * kRgWarpSmem;
-  rp.sub_shift = 0;
-  while ((n - 1) >> rp.sub_shift >= 4) ++rp.sub_shift;
   rp.grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(rows, (uint64_t)sm_count() * cps));
   rp.ok = true;
   return rp;
@@ -67,8 +65,8 @@ void run_rowreg(const RgPlan& rp, const void* in, uint64_t rows, uint32_t k, flo
   RgArgs a{};
   a.in = static_cast<const uint16_t*>(in);
   a.rows = rows;
+  a.S = rp.S;
   a.k = k;
-  a.sub_shift = rp.sub_shift;
   a.margin = (uint32_t)opt("rowreg_margin", 5);
   a.force = (uint32_t)opt("rowreg_force", 0);
   a.probe = (uint32_t)opt("rowreg_probe", 0);
@@ -76,12 +74,13 @@ void run_rowreg(const RgPlan& rp, const void* in, uint64_t rows, uint32_t k, flo
   a.out_i = oi;
   a.status = status;
   g_prof.bracket_begin(st);
-  switch (rp.S) {
-    case 28: rg_dispatch<28>(rp, a, st); break;
-    case 56: rg_dispatch<56>(rp, a, st); break;
-    case 112: rg_dispatch<112>(rp, a, st); break;
-    default: rg_dispatch<128>(rp, a, st); break;
-  }
+  // unrolled instantiations for the common row lengths, else the row length as a run-time argument
+  const bool rt = opt("rowreg_rt", 0) != 0;
+  if (rp.S == 112 && !rt) rg_dispatch<112>(rp, a, st);
+  else if (rp.S == 128 && !rt) rg_dispatch<128>(rp, a, st);
+  else if (rp.S == 56 && !rt) rg_dispatch<56>(rp, a, st);
+  else if (rp.S == 28 && !rt) rg_dispatch<28>(rp, a, st);
+  else rg_dispatch<0>(rp, a, st);
   g_prof.bracket_end(st);
 }
 

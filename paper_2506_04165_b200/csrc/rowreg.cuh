@@ -55,8 +55,8 @@ static_assert(8 * 256 == 4 * kRgTmp, "the sorted keys reuse the staging tile");
 struct RgArgs {
   const uint16_t* in;
   uint64_t rows;
+  uint32_t S;           // stride-rows per bucket (n = 128 S)
   uint32_t k;
-  uint32_t sub_shift;   // pos >> sub_shift < 4
   uint32_t margin;      // prediction: codes below the level of the last row's K-th candidate
   uint32_t force;       // tests: 1 = every row two-pass, 2 = every row exact
   uint32_t probe;       // development: stop after phase `probe`
@@ -237,6 +237,106 @@ __device__ __forceinline__ void rg_max(const uint2* p, uint32_t (&gm)[2][4]) {
   }
 }
 
+// The same two passes for a row length known only at run time (S = 0
+// instantiation: any 8 <= S <= 512): tiles in pairs through two register
+// buffers, the ragged last tile with per-stride-row checks.
+template <bool POS>
+__device__ __forceinline__ void rg_hits_rt(const uint2* p, const uint8_t* nxt, int S, uint32_t L2, uint32_t lane,
+                                           uint2* stage, uint4* state, uint32_t& nan) {
+  constexpr int AH = 3;
+  constexpr uint32_t TB = kRgTile * 256;
+  const int NB = (S + kRgTile - 1) / kRgTile;
+  const uint8_t* rowb = reinterpret_cast<const uint8_t*>(p) - 8 * lane;
+  const uint8_t* col = reinterpret_cast<const uint8_t*>(stage + lane);
+  uint4* st4 = state + 4 * lane;
+  // a stride-row past the end loads as -inf: never a hit (the level is above -inf)
+  auto load = [&](uint2 (&b)[kRgTile], int t) {
+    const int s0 = t * kRgTile;
+    const uint2* pt = p + s0 * 32;  // immediate offsets from one pointer per tile
+    if (s0 + kRgTile <= S) {
+#pragma unroll
+      for (int i = 0; i < kRgTile; ++i) b[i] = rg_ldg(pt + i * 32);
+    } else {
+#pragma unroll
+      for (int i = 0; i < kRgTile; ++i) {
+        b[i] = make_uint2(0xff80ff80u, 0xff80ff80u);
+        if (s0 + i < S) b[i] = rg_ldg(pt + i * 32);
+      }
+    }
+  };
+  uint2* stl = stage + lane;
+  auto process = [&](const uint2 (&b)[kRgTile], int t) {
+    {
+      const int ta = t + AH;
+      const uint32_t off = (uint32_t)(ta < NB ? ta : ta - NB) * TB + lane * 128;
+      const uint8_t* q = ta < NB ? rowb : nxt;
+      if (lane < TB / 128 && q && off < (uint32_t)S * 256) asm volatile("prefetch.global.L2 [%0];" ::"l"(q + off));
+    }
+    const int s0 = t * kRgTile;
+    uint32_t ax = 0x3f803f80u, ay = 0x3f803f80u;
+#pragma unroll
+    for (int i = 0; i < kRgTile; ++i) {
+      ax = rg_shl_add(ax, rg_geu1(b[i].x, L2));
+      ay = rg_shl_add(ay, rg_geu1(b[i].y, L2));
+      stl[(6 - i) * 32] = b[i];
+    }
+    uint32_t m = (ax & 0x007f007fu) | ((ay & 0x007f007fu) << 8);
+    const uint32_t pbase = ((uint32_t)(s0 + 6) << 7) + 4 * lane;
+    while (m) {
+      uint32_t bb;
+      asm("bfind.u32 %0, %1;" : "=r"(bb) : "r"(m));
+      m ^= 1u << bb;
+      const uint32_t r = bb & 7u;
+      const uint32_t j = ((bb >> 2) & 2u) | (bb >> 4);
+      uint32_t val = *reinterpret_cast<const uint16_t*>(col + r * 256 + j * 2);
+      if (!POS) {
+        if ((val & 0x7fffu) > 0x7f80u) nan = 1u;
+        val = asc_code16(val);
+      }
+      const uint32_t e = (val << 16) | (pbase - (r << 7) + j);
+      uint4 sv = st4[j];
+      if (sv.w <= (e | 0xffffu)) {
+        const uint32_t eb = e & 0xffff0000u;
+        const bool a2 = sv.z >= eb, a1 = sv.y >= eb, a0 = sv.x >= eb;
+        sv.w = a2 ? e : sv.z;
+        sv.z = a2 ? sv.z : (a1 ? e : sv.y);
+        sv.y = a1 ? sv.y : (a0 ? e : sv.x);
+        sv.x = a0 ? sv.x : e;
+        st4[j] = sv;
+      }
+    }
+  };
+  uint2 b0[kRgTile], b1[kRgTile];
+  load(b0, 0);
+#pragma unroll 1
+  for (int bt = 0; bt < NB; bt += 2) {
+    if (bt + 1 < NB) load(b1, bt + 1);
+    process(b0, bt);
+    if (bt + 1 < NB) {
+      if (bt + 2 < NB) load(b0, bt + 2);
+      process(b1, bt + 1);
+    }
+  }
+}
+
+__device__ __forceinline__ void rg_max_rt(const uint2* p, int S, uint32_t (&gm)[2][4]) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const int s1 = g == 3 ? S : (g + 1) * S / 4;
+#pragma unroll 1
+    for (int s = g * S / 4; s < s1; s += 4) {
+      uint2 v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = s + i < s1 ? rg_ldg(p + (s + i) * 32) : make_uint2(0xff80ff80u, 0xff80ff80u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        gm[0][g] = bmax_nan(gm[0][g], v[i].x);
+        gm[1][g] = bmax_nan(gm[1][g], v[i].y);
+      }
+    }
+  }
+}
+
 // lane count of the 16 group maxima >= L2 (float order)
 __device__ __forceinline__ uint32_t rg_count_ge(const uint32_t (&gm)[2][4], uint32_t L2) {
   uint32_t t = 0;
@@ -250,8 +350,7 @@ __device__ __forceinline__ uint32_t rg_count_ge(const uint32_t (&gm)[2][4], uint
 // The exact path (degenerate rows): Alg. 1 of every bucket as the reference
 // runs it (topk.cpp:80-102 with the {-inf, 0} sentinels of topk.cpp:118-121),
 // the B K' = 512 rank keys sorted, the first K written (topk.cpp:192-236).
-template <int S>
-__device__ __noinline__ void rg_exact(const uint16_t* xr, uint32_t lane, uint32_t K, uint64_t* srt, float* ov,
+__device__ __noinline__ void rg_exact(const uint16_t* xr, int S, uint32_t lane, uint32_t K, uint64_t* srt, float* ov,
                                       uint32_t* oi) {
 #pragma unroll 1
   for (int j = 0; j < 4; ++j) {
@@ -290,13 +389,21 @@ __device__ __noinline__ void rg_exact(const uint16_t* xr, uint32_t lane, uint32_
   __syncwarp();
 }
 
-// S = stride-rows (n = 128 S <= 16384), B = 128, K' = 4.  CPS CTAs of NW warps per SM;
+template <int S, bool POS, int PF>
+__device__ __forceinline__ void rg_hits_any(const uint2* p, const uint8_t* nxt, int Sx, uint32_t L2, uint32_t lane,
+                                            uint2* stage, uint4* state, uint32_t& nan) {
+  if constexpr (S != 0) rg_hits<S, POS, PF>(p, nxt, L2, lane, stage, state, nan);
+  else rg_hits_rt<POS>(p, nxt, Sx, L2, lane, stage, state, nan);
+}
+
+// S = stride-rows (n = 128 S <= 65536; 0 = a run-time argument), B = 128, K' = 4.  CPS CTAs of NW warps per SM;
 // CTA c owns the rows [rows c / G, rows (c + 1) / G) and its warps pull them
 // from a shared counter.  `pred` is the CTA's prediction (an ascending code;
 // ~0 = none).
 template <int S, int NW, int PF, int CPS>
 __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
-  constexpr uint32_t n = 128u * S;
+  const int Sx = S ? S : (int)a.S;  // S = 0: the row length is a run-time argument
+  const uint32_t n = 128u * (uint32_t)Sx;
   extern __shared__ __align__(128) uint8_t rg_smem[];
   __shared__ uint32_t queue;
   __shared__ volatile uint32_t pred;
@@ -323,8 +430,8 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       pm[0][g] = pm[1][g] = 0xff80ff80u;
-      const int s1 = g == 3 ? S : (g + 1) * S / 4;
-      for (int s = g * S / 4 + (int)wid; s < s1; s += NW) {
+      const int s1 = g == 3 ? Sx : (g + 1) * Sx / 4;
+      for (int s = g * Sx / 4 + (int)wid; s < s1; s += NW) {
         const uint2 v = rg_ldg(p0 + s * 32);
         pm[0][g] = bmax_nan(pm[0][g], v.x);
         pm[1][g] = bmax_nan(pm[1][g], v.y);
@@ -402,8 +509,8 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
     uint32_t M = 0, nan = 0;
     if (have) {
       clear_state();
-      if (posmode) rg_hits<S, true, PF>(p, nxt, rg_bits2(Lkey), lane, stage, state, nan);
-      else rg_hits<S, false, PF>(p, nxt, rg_bits2(Lkey), lane, stage, state, nan);
+      if (posmode) rg_hits_any<S, true, PF>(p, nxt, Sx, rg_bits2(Lkey), lane, stage, state, nan);
+      else rg_hits_any<S, false, PF>(p, nxt, Sx, rg_bits2(Lkey), lane, stage, state, nan);
       M = filled();
     }
     if (a.probe == 1) {  // development: the pass alone (its results consumed)
@@ -420,7 +527,8 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
       for (int w = 0; w < 2; ++w)
 #pragma unroll
         for (int g = 0; g < 4; ++g) gm[w][g] = 0xff80ff80u;
-      rg_max<S>(p, gm);
+      if constexpr (S != 0) rg_max<S>(p, gm);
+      else rg_max_rt(p, Sx, gm);
       const uint32_t mm = bmax_nan(bmax_nan(bmax_nan(gm[0][0], gm[0][1]), bmax_nan(gm[0][2], gm[0][3])),
                                    bmax_nan(bmax_nan(gm[1][0], gm[1][1]), bmax_nan(gm[1][2], gm[1][3])));
       nan = ((mm & 0x7fffu) > 0x7f80u || ((mm >> 16) & 0x7fffu) > 0x7f80u) ? 1u : 0u;
@@ -441,15 +549,15 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
       } else {
         posmode = Lkey > 0x8000u;
         clear_state();
-        if (posmode) rg_hits<S, true, PF>(p, nxt, rg_bits2(Lkey), lane, stage, state, nan);
-        else rg_hits<S, false, PF>(p, nxt, rg_bits2(Lkey), lane, stage, state, nan);
+        if (posmode) rg_hits_any<S, true, PF>(p, nxt, Sx, rg_bits2(Lkey), lane, stage, state, nan);
+        else rg_hits_any<S, false, PF>(p, nxt, Sx, rg_bits2(Lkey), lane, stage, state, nan);
         M = filled();
       }
     }
     if (a.probe == 2) continue;
     if (exact) {
       __syncwarp();
-      rg_exact<S>(xr, lane, K, reinterpret_cast<uint64_t*>(wsm), ov, oi);  // tile | state: 4 KB
+      rg_exact(xr, Sx, lane, K, reinterpret_cast<uint64_t*>(wsm), ov, oi);  // tile | state: 4 KB
       continue;
     }
     __syncwarp();

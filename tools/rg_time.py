@@ -49,6 +49,21 @@ def main():
                         line(f"  warps={w} probe {pr} ({what})", timeit(run))
             with opt("rowreg_force", 1):
                 line(f"  warps={w} every row two-pass", timeit(run))
+    with opt("rowreg_rt", 1):
+        line("rowreg, run-time row length (S = 0 instantiation)", timeit(run))
+    if "--shapes" in sys.argv:  # other row lengths (run-time S) against the previous kernels
+        for n2, k2 in [(3584, 100), (7168, 287), (11008, 220), (16384, 300), (28672, 287), (65536, 512)]:
+            rows2 = max(1024, (235 << 20) // (2 * n2))
+            x2 = torch.randn(rows2, n2, device=dev).to(torch.bfloat16)
+            out2 = (torch.empty(rows2, k2, device=dev), torch.empty(rows2, k2, dtype=torch.int32, device=dev))
+            p2 = atk.AlgoParams(n2, 128, 4, k2)
+            run2 = lambda: atk.approx_top_k_device(x2, p2, status=st, out=out2)  # noqa: E731
+            t_new = timeit(run2, iters=20)
+            with opt("rowreg", 0):
+                t_old = timeit(run2, iters=5)
+            gb = rows2 * n2 * 2 / 1e3
+            print(f"n={n2:6d} K={k2:3d} rows={rows2:6d}: rowreg {t_new:8.1f} us ({gb / t_new / 6552.3:.3f} of peak)  previous {t_old:8.1f} us", flush=True)
+            del x2
     if "--stats" in sys.argv:
         for m in [1, 2, 3, 5, 8, 12]:
             with opt("rowreg_margin", m), opt("rowreg_probe", 9):
