@@ -818,6 +818,11 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
       run_rowreg(rgp, d_in, rows, p->global_k, d_out_vals, d_out_idx, d_status, st);
       return;
     }
+    const RgPlan rxp = plan_rowregx(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
+    if (rxp.ok) {  // the C3 sweep shapes with 1024 candidates per row (rowregx.cuh)
+      run_rowregx(rxp, d_in, rows, p->num_buckets, p->local_k, p->global_k, d_out_vals, d_out_idx, d_status, st);
+      return;
+    }
     const StPlan sp = plan_streamthr(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
     if (sp.ok) {  // long rows: threshold stream + per-row finish (exact fallback per row)
       void* sws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(d_ws)));

@@ -121,6 +121,11 @@ RgPlan plan_rowreg(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_
                    bool for_size = false);
 void run_rowreg(const RgPlan& rp, const void* in, uint64_t rows, uint32_t k, float* ov, uint32_t* oi,
                 uint32_t* status, cudaStream_t st);
+// the same stream for the C3 sweep shapes with 1024 candidates per row (rowregx.cu)
+RgPlan plan_rowregx(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
+                    bool for_size = false);
+void run_rowregx(const RgPlan& rp, const void* in, uint64_t rows, uint64_t B, uint32_t kp, uint32_t k, float* ov,
+                 uint32_t* oi, uint32_t* status, cudaStream_t st);
 
 // stage 2 by counting-sort ranks for 128 < count <= 1024 (streamthr.cu);
 // false if not applicable

@@ -350,7 +350,7 @@ __device__ __forceinline__ uint32_t rg_count_ge(const uint32_t (&gm)[2][4], uint
 // The exact path (degenerate rows): Alg. 1 of every bucket as the reference
 // runs it (topk.cpp:80-102 with the {-inf, 0} sentinels of topk.cpp:118-121),
 // the B K' = 512 rank keys sorted, the first K written (topk.cpp:192-236).
-__device__ __noinline__ void rg_exact(const uint16_t* xr, int S, uint32_t lane, uint32_t K, uint64_t* srt, float* ov,
+static __device__ __noinline__ void rg_exact(const uint16_t* xr, int S, uint32_t lane, uint32_t K, uint64_t* srt, float* ov,
                                       uint32_t* oi) {
 #pragma unroll 1
   for (int j = 0; j < 4; ++j) {
