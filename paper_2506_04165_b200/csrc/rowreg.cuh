@@ -49,7 +49,8 @@ constexpr uint32_t kRgKeyNegInf = 0x007fu;   // asc_code16(-inf)
 constexpr int kRgTile = 7;                   // stride-rows per load batch = per staging tile (7 hit bits per
                                              // bucket and tile fit a bf16 counter exactly: 128 + bits)
 // per warp: staging tile [8][32] x 8 B (the sorted keys after the pass) | state [128 buckets][4] u32
-constexpr uint32_t kRgWarpSmem = 8 * 256 + 4 * 512;
+constexpr uint32_t kRgLaneQ = 5;            // uint4 per lane in the state: 4 buckets + 16 bytes of padding (banks)
+constexpr uint32_t kRgWarpSmem = 8 * 256 + 16 * kRgLaneQ * 32;
 static_assert(8 * 256 == 4 * kRgTmp, "the sorted keys reuse the staging tile");
 
 struct RgArgs {
@@ -157,7 +158,7 @@ __device__ __forceinline__ void rg_hits(const uint2* p, const uint8_t* nxt, uint
       if (i < S) buf[0][i] = rg_ldg(p + i * 32);
   }
   const uint8_t* col = reinterpret_cast<const uint8_t*>(stage + lane);
-  uint4* st4 = state + 4 * lane;  // the lane's buckets 4 lane .. 4 lane + 3
+  uint4* st4 = state + kRgLaneQ * lane;  // the lane's buckets 4 lane .. 4 lane + 3
 #pragma unroll
   for (int bt = 0; bt < NB; ++bt) {
     if (bt + PF < NB) {
@@ -248,7 +249,7 @@ __device__ __forceinline__ void rg_hits_rt(const uint2* p, const uint8_t* nxt, i
   const int NB = (S + kRgTile - 1) / kRgTile;
   const uint8_t* rowb = reinterpret_cast<const uint8_t*>(p) - 8 * lane;
   const uint8_t* col = reinterpret_cast<const uint8_t*>(stage + lane);
-  uint4* st4 = state + 4 * lane;
+  uint4* st4 = state + kRgLaneQ * lane;
   // a stride-row past the end loads as -inf: never a hit (the level is above -inf)
   auto load = [&](uint2 (&b)[kRgTile], int t) {
     const int s0 = t * kRgTile;
@@ -490,14 +491,14 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
     // ---- the hit pass against the prediction: Alg. 1 over the hits ---------
     auto clear_state = [&]() {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) state[4 * lane + j] = make_uint4(0, 0, 0, 0);
+      for (int j = 0; j < 4; ++j) state[kRgLaneQ * lane + j] = make_uint4(0, 0, 0, 0);
     };
     // M = sum_b min(K', c_b) = the filled slots
     auto filled = [&]() {
       uint32_t f = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const uint4 sv = state[4 * lane + j];
+        const uint4 sv = state[kRgLaneQ * lane + j];
         f += (sv.x ? 1u : 0u) + (sv.y ? 1u : 0u) + (sv.z ? 1u : 0u) + (sv.w ? 1u : 0u);
       }
       return __reduce_add_sync(0xffffffffu, f);
@@ -572,7 +573,7 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
       uint32_t k[16];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const uint4 sv = state[4 * lane + j];
+        const uint4 sv = state[kRgLaneQ * lane + j];
         k[4 * j] = sv.x ^ 0xffff0000u;
         k[4 * j + 1] = sv.y ^ 0xffff0000u;
         k[4 * j + 2] = sv.z ^ 0xffff0000u;
@@ -617,12 +618,17 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
           }
         }
       }
+      // sorted element x = 16 lane + i goes to tq[(x / 16) * 20 + x % 16]: 80-byte lane stride
+      // (16-byte stores without bank conflicts) over the dead staging tile and state
       __syncwarp();
+      uint32_t* tq = tmp;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) tmp[16 * lane + i] = k[i];
+      for (int q = 0; q < 4; ++q)
+        reinterpret_cast<uint4*>(tq)[kRgLaneQ * lane + q] = make_uint4(k[4 * q], k[4 * q + 1], k[4 * q + 2], k[4 * q + 3]);
       __syncwarp();
+      auto sorted = [&](uint32_t x) { return tq[(x >> 4) * (4 * kRgLaneQ) + (x & 15u)]; };
       // a NaN element was a hit (unordered compare): as raw bits it sorts first
-      if (posmode && ((~(tmp[0] >> 16)) & 0x7fffu) > 0x7f80u) nan = 1u;
+      if (posmode && ((~(sorted(0) >> 16)) & 0x7fffu) > 0x7f80u) nan = 1u;
       if (__reduce_or_sync(0xffffffffu, nan)) {  // the reference rejects the input
         if (lane == 0) atomicOr(a.status, ATKG_FLAG_NAN);
         continue;
@@ -634,12 +640,12 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
         }
       } else {
         for (uint32_t x = lane; x < K; x += 32) {
-          const uint32_t key = tmp[x], code = ~(key >> 16) & 0xffffu;
+          const uint32_t key = sorted(x), code = ~(key >> 16) & 0xffffu;
           ov[x] = __uint_as_float((posmode ? code : code16_bits(code)) << 16);
           oi[x] = key & 0xffffu;
         }
       }
-      const uint32_t ck = ~(tmp[K - 1] >> 16) & 0xffffu;  // the K-th candidate's level
+      const uint32_t ck = ~(sorted(K - 1) >> 16) & 0xffffu;  // the K-th candidate's level
       Lstar = posmode ? (ck | 0x8000u) : ck;
     }
     // the next rows' prediction (a racing update by another warp is as good)
