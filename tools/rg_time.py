@@ -73,9 +73,10 @@ def main():
                 tp, msum = out[1].view(-1)[:2].tolist()
                 print(f"margin={m}: two-pass rows {tp} of {rows}, mean M {msum / rows:.1f}", flush=True)
     if "--sweep" in sys.argv:
-        for m in [1, 2, 3, 4, 5, 6, 8, 12]:
-            with opt("rowreg_margin", m):
-                line(f"margin={m}", timeit(run))
+        for rep in range(2):
+            for m in [7, 8, 9, 10, 12, 14, 16, 20]:
+                with opt("rowreg_margin", m), opt("rowreg_warps", 29):
+                    line(f"margin={m} (warps=29, pass {rep})", timeit(run, iters=100))
     with opt("rowreg", 0):
         line("row_resident_kernel (previous default)", timeit(run, iters=20))
     atk.check_status(st)
