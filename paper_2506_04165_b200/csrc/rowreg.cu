@@ -51,7 +51,10 @@ RgPlan plan_rowreg(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_
   if (reinterpret_cast<uintptr_t>(in) % 8 != 0) return rp;
   rp.S = (uint32_t)S;
   // warps per CTA (= per SM); 29 / 33 = 28 / 32 warps with the loads issued one tile ahead
-  uint32_t w = (uint32_t)opt("rowreg_warps", 29);
+  // the unrolled instantiations run best at 28 warps with the loads one tile ahead (72 registers); the
+  // run-time row length needs 96 registers to keep its addresses (20 warps: 71 us vs 84 us on the C3 shape)
+  const bool unrolled = S == 112 || S == 128 || S == 56 || S == 28;
+  uint32_t w = (uint32_t)opt("rowreg_warps", unrolled && !opt("rowreg_rt", 0) ? 29 : 20);
   rp.warps = w <= 12 ? 12 : w <= 16 ? 16 : w <= 20 ? 20 : w <= 24 ? 24 : w <= 28 ? 28 : w == 29 ? 29 : w <= 32 ? 32 : w == 33 ? 33 : w <= 36 ? 36 : 40;
   const uint32_t cps = rp.warps > 33 ? 2 : 1;
   rp.smem = (size_t)(rp.warps == 29 ? 28 : rp.warps == 33 ? 32 : rp.warps / cps) * kRgWarpSmem;
