@@ -680,6 +680,8 @@ size_t ws_need_uncached(int op, int dtype, uint64_t rows, const atkg_params& pr)
         if (rwp.ok) b = std::max<size_t>(b, rwp.ws_bytes);
         const SrPlan srp = plan_short(dtype, in, rows, p->n, p->num_buckets, p->local_k, p->global_k, true);
         if (srp.ok) b = std::max<size_t>(b, srp.ws_bytes);
+        const RmPlan rmp = plan_rowmax1(dtype, in, rows, p->n, p->num_buckets, p->local_k, p->global_k, true);
+        if (rmp.ok) b = std::max<size_t>(b, rmp.ws_bytes + 256);
         break;
       }
       case ATKG_OP_SELECT:
@@ -816,6 +818,12 @@ int atkg_approx_top_k(int dtype, const void* d_in, uint64_t rows, const atkg_par
     const RgPlan rgp = plan_rowreg(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
     if (rgp.ok) {  // bf16 rows up to 65536 with B = 128, K' = 4: one warp per row, streamed once into registers (rowreg.cuh)
       run_rowreg(rgp, d_in, rows, p->global_k, d_out_vals, d_out_idx, d_status, st);
+      return;
+    }
+    const RmPlan rmp = plan_rowmax1(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);
+    if (rmp.ok) {  // K' = 1 with buckets of 2-8 elements: the register row stream, exact kernel for the rest
+      run_rowmax1(rmp, dtype, d_in, rows, p->n, p->num_buckets, p->global_k, d_out_vals, d_out_idx,
+                  reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(d_ws))), d_status, st);
       return;
     }
     const RgPlan rxp = plan_rowregx(dtype, d_in, rows, p->n, p->num_buckets, p->local_k, p->global_k);

@@ -96,8 +96,23 @@ struct SrPlan {
 };
 SrPlan plan_short(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
                   bool for_size = false);
+// row_list / row_count (device): only those rows (the rows rowmax1.cu could not settle)
 void run_short(int dtype, const SrPlan& sp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
-               uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
+               uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st,
+               const uint32_t* row_list = nullptr, const uint32_t* row_count = nullptr);
+
+// K' = 1 on the register row stream; the rows it cannot settle go to run_short (rowmax1.cu)
+struct RmPlan {
+  bool ok = false;
+  uint32_t S = 0, cpl = 0, warps = 0, grid = 0;
+  size_t smem = 0;
+  SrPlan fallback;
+  uint64_t ws_bytes = 0;  // the fallback's scratch | counter | row list
+};
+RmPlan plan_rowmax1(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp, uint32_t k,
+                    bool for_size = false);
+void run_rowmax1(const RmPlan& rp, int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t k,
+                 float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st);
 
 // one warp per bf16 row held in shared memory (rowwarp.cu)
 struct RwPlan {

@@ -97,7 +97,8 @@ SrPlan plan_short(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_t
 }
 
 void run_short(int dtype, const SrPlan& sp, const void* in, uint64_t rows, uint64_t n, uint64_t B, uint32_t kp,
-               uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st) {
+               uint32_t k, float* ov, uint32_t* oi, void* ws, uint32_t* status, cudaStream_t st,
+               const uint32_t* row_list, const uint32_t* row_count) {
   (void)dtype;
   SrArgs a{};
   a.in = in;
@@ -117,6 +118,8 @@ void run_short(int dtype, const SrPlan& sp, const void* in, uint64_t rows, uint6
   a.force_slow = (uint32_t)opt("short_force_slow", 0);
   a.probe = (uint32_t)opt("short_probe", 0);
   a.gws = static_cast<uint64_t*>(ws);
+  a.row_list = row_list;
+  a.row_count = row_count;
   a.out_v = ov;
   a.out_i = oi;
   a.status = status;

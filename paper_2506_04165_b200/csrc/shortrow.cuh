@@ -75,6 +75,8 @@ struct SrArgs {
   uint32_t force_slow;  // tests: every row takes the exact path
   uint32_t probe;       // development: stream the rows only
   uint64_t* gws;        // exact path scratch, [grid][P]
+  const uint32_t* row_list;   // optional: only these rows (rowmax1.cuh leaves it the rows it could not settle)
+  const uint32_t* row_count;  //           how many (device)
   float* out_v;
   uint32_t* out_i;
   uint32_t* status;
@@ -153,23 +155,26 @@ __global__ void __launch_bounds__(kSrThreads) short_row_kernel(SrArgs a) {
     ptx::fence_mbar_init();
   }
   __syncthreads();
-  uint64_t row = blockIdx.x;
-  if (t == 0 && row < a.rows) {
+  const uint64_t nwork = a.row_list ? (uint64_t)*a.row_count : a.rows;
+  auto row_of = [&](uint64_t i) { return a.row_list ? (uint64_t)a.row_list[i] : i; };
+  uint64_t widx = blockIdx.x;
+  if (t == 0 && widx < nwork) {
     ptx::mbar_arrive_expect_tx(&bar[0], a.row_bytes);
-    ptx::bulk_g2s(slots, in + row * a.row_bytes, a.row_bytes, &bar[0], pol);
+    ptx::bulk_g2s(slots, in + row_of(widx) * a.row_bytes, a.row_bytes, &bar[0], pol);
   }
 #pragma unroll 1
-  for (uint32_t it = 0; row < a.rows; ++it, row += gridDim.x) {
+  for (uint32_t it = 0; widx < nwork; ++it, widx += gridDim.x) {
+    const uint64_t row = row_of(widx);
     const uint32_t s = it & 1;
     uint8_t* rowp = slots + (size_t)s * a.slot_bytes;
     const uint2* ch = reinterpret_cast<const uint2*>(rowp);
     const uint16_t* xh = reinterpret_cast<const uint16_t*>(rowp);
     {  // the next row into the other slot (its last use ended at the previous barrier)
-      const uint64_t nrow = row + gridDim.x;
-      if (t == 0 && nrow < a.rows) {
+      const uint64_t nidx = widx + gridDim.x;
+      if (t == 0 && nidx < nwork) {
         ptx::mbar_arrive_expect_tx(&bar[s ^ 1], a.row_bytes);
-        ptx::bulk_g2s(slots + (size_t)(s ^ 1) * a.slot_bytes, in + nrow * a.row_bytes, a.row_bytes, &bar[s ^ 1],
-                      pol);
+        ptx::bulk_g2s(slots + (size_t)(s ^ 1) * a.slot_bytes, in + row_of(nidx) * a.row_bytes, a.row_bytes,
+                      &bar[s ^ 1], pol);
       }
     }
     hist[t & 255] = 0;
