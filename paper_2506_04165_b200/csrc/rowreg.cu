@@ -19,21 +19,15 @@ void rg_launch(const RgPlan& rp, const RgArgs& a, cudaStream_t st) {
   check_launch();
 }
 
-// rp.warps = warps per SM; 29 / 33 = 28 / 32 warps with the loads issued one tile ahead;
-// above 32 as two CTAs per SM
+// rp.warps = warps per SM (one CTA): 29 / 33 = 28 / 32 warps with the loads issued one tile ahead
 template <int S>
 void rg_dispatch(const RgPlan& rp, const RgArgs& a, cudaStream_t st) {
   switch (rp.warps) {
-    case 12: rg_launch<S, 12, 1, 1>(rp, a, st); break;
     case 16: rg_launch<S, 16, 1, 1>(rp, a, st); break;
     case 20: rg_launch<S, 20, 1, 1>(rp, a, st); break;
     case 24: rg_launch<S, 24, 1, 1>(rp, a, st); break;
-    case 28: rg_launch<S, 28, 0, 1>(rp, a, st); break;
     case 29: rg_launch<S, 28, 1, 1>(rp, a, st); break;
-    case 32: rg_launch<S, 32, 0, 1>(rp, a, st); break;
-    case 33: rg_launch<S, 32, 1, 1>(rp, a, st); break;
-    case 36: rg_launch<S, 18, 0, 2>(rp, a, st); break;
-    default: rg_launch<S, 20, 0, 2>(rp, a, st); break;
+    default: rg_launch<S, 32, 1, 1>(rp, a, st); break;
   }
 }
 
@@ -55,9 +49,9 @@ RgPlan plan_rowreg(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_
   // run-time row length needs 96 registers to keep its addresses (20 warps: 71 us vs 84 us on the C3 shape)
   const bool unrolled = S == 112 || S == 128 || S == 56 || S == 28;
   uint32_t w = (uint32_t)opt("rowreg_warps", unrolled && !opt("rowreg_rt", 0) ? 29 : 20);
-  rp.warps = w <= 12 ? 12 : w <= 16 ? 16 : w <= 20 ? 20 : w <= 24 ? 24 : w <= 28 ? 28 : w == 29 ? 29 : w <= 32 ? 32 : w == 33 ? 33 : w <= 36 ? 36 : 40;
-  const uint32_t cps = rp.warps > 33 ? 2 : 1;
-  rp.smem = (size_t)(rp.warps == 29 ? 28 : rp.warps == 33 ? 32 : rp.warps / cps) * kRgWarpSmem;
+  rp.warps = w <= 16 ? 16 : w <= 20 ? 20 : w <= 24 ? 24 : w <= 29 ? 29 : 33;
+  const uint32_t cps = 1;
+  rp.smem = (size_t)(rp.warps == 29 ? 28 : rp.warps == 33 ? 32 : rp.warps) * kRgWarpSmem;
   rp.grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(rows, (uint64_t)sm_count() * cps));
   rp.ok = true;
   return rp;
