@@ -48,7 +48,22 @@ RgPlan plan_rowreg(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_
   // the unrolled instantiations run best at 28 warps with the loads one tile ahead (72 registers); the
   // run-time row length needs 96 registers to keep its addresses (20 warps: 71 us vs 84 us on the C3 shape)
   const bool unrolled = S == 112 || S == 128 || S == 56 || S == 28;
-  uint32_t w = (uint32_t)opt("rowreg_warps", unrolled && !opt("rowreg_rt", 0) ? 29 : 20);
+  uint32_t w = (uint32_t)opt("rowreg_warps", 0);
+  if (w == 0) {
+    if (!unrolled || opt("rowreg_rt", 0)) {
+      w = 20;
+    } else {
+      // every warp runs whole rows one after the other and the kernel is issue-bound, so its time goes
+      // with waves x warps: the warp count with the fewest idle warp-rows per SM (ties: more warps)
+      const uint64_t rps = (rows + (uint64_t)sm_count() - 1) / (uint64_t)sm_count();
+      uint64_t best = ~0ull;
+      for (uint32_t c : {16u, 20u, 24u, 28u}) {
+        const uint64_t cost = (rps + c - 1) / c * c;
+        if (cost <= best) { best = cost; w = c; }
+      }
+      if (w == 28) w = 29;  // 28 warps: the loads one tile ahead fit in 72 registers
+    }
+  }
   rp.warps = w <= 16 ? 16 : w <= 20 ? 20 : w <= 24 ? 24 : w <= 29 ? 29 : 33;
   const uint32_t cps = 1;
   rp.smem = (size_t)(rp.warps == 29 ? 28 : rp.warps == 33 ? 32 : rp.warps) * kRgWarpSmem;
