@@ -36,12 +36,14 @@ RgPlan plan_rowregx(int dtype, const void* in, uint64_t rows, uint64_t n, uint64
   RgPlan rp;
   if (!for_size && (!opt("rowregx", 1) || opt("short", 0) || opt("rowwarp", 0))) return rp;
   if (dtype != ATKG_BF16 || n != 14336) return rp;
-  if (!((kp == 2 && B == 512) || (kp == 4 && B == 256) || (kp == 8 && B == 128))) return rp;
+  const bool big = kp == 2 && B == 1024;  // 2048 candidates: 64 slots per lane, 20 warps
+  if (!((kp == 2 && B == 512) || (kp == 4 && B == 256) || (kp == 8 && B == 128) || big)) return rp;
   if (k > 1024 || reinterpret_cast<uintptr_t>(in) % 8 != 0) return rp;
   rp.S = (uint32_t)(n / B);
-  const uint32_t w = (uint32_t)opt("rowregx_warps", 28);
-  rp.warps = w <= 16 ? 16 : w <= 20 ? 20 : w <= 24 ? 24 : 28;
-  rp.smem = (size_t)rp.warps * rx_warp_smem<4, 2>();  // the same for the three shapes (K' CPL = 8)
+  const uint32_t w = (uint32_t)opt("rowregx_warps", big ? 20 : 28);
+  rp.warps = w <= 16 ? 16 : w <= 20 || big ? 20 : w <= 24 ? 24 : 28;
+  // the same for the three 1024-candidate shapes (K' CPL = 8)
+  rp.smem = (size_t)rp.warps * (big ? rx_warp_smem<2, 8>() : rx_warp_smem<4, 2>());
   rp.grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(rows, (uint64_t)sm_count()));
   rp.ok = true;
   return rp;
@@ -60,9 +62,11 @@ void run_rowregx(const RgPlan& rp, const void* in, uint64_t rows, uint64_t B, ui
   a.out_v = ov;
   a.out_i = oi;
   a.status = status;
-  (void)B;
   g_prof.bracket_begin(st);
-  if (kp == 2) rx_dispatch<28, 2, 4>(rp, a, st);
+  if (kp == 2 && B == 1024) {
+    if (rp.warps == 16) rx_launch<14, 2, 8, 16>(rp, a, st);
+    else rx_launch<14, 2, 8, 20>(rp, a, st);
+  } else if (kp == 2) rx_dispatch<28, 2, 4>(rp, a, st);
   else if (kp == 4) rx_dispatch<56, 4, 2>(rp, a, st);
   else rx_dispatch<112, 8, 1>(rp, a, st);
   g_prof.bracket_end(st);

@@ -1,7 +1,8 @@
 // rowregx.cuh -- the register row stream of rowreg.cuh for the other bucket
 // shapes of the C3 K' sweep (BASELINE configs[2]): K' in {2, 4, 8} with
 // B = 128 CPL buckets, CPL in {1, 2, 4}, B K' = 1024 candidates per row
-// (K' = 2 / B = 512, K' = 4 / B = 256, K' = 8 / B = 128).
+// (K' = 2 / B = 512, K' = 4 / B = 256, K' = 8 / B = 128), and K' = 2 / B = 1024
+// (2048 candidates: 64 slots per lane, packed to <= 32 before the sort).
 //
 // Same design, generalised (rowreg.cuh has the argument and the references):
 //   * one warp per row; lane l owns the 4 CPL buckets 4 (l + 32 k) + j of the
@@ -159,11 +160,14 @@ __device__ __forceinline__ void rx_max(const uint2* p, uint32_t (&gm)[2 * CPL * 
 
 template <int NG>
 __device__ __forceinline__ uint32_t rx_count_ge(const uint32_t (&gm)[NG], uint32_t L2) {
-  static_assert(NG <= 16, "one bit pair per register");
-  uint32_t t = 0;
+  static_assert(NG <= 32, "one bit pair per register, two accumulators");
+  uint32_t t0 = 0, t1 = 0;
 #pragma unroll
-  for (int i = 0; i < NG; ++i) t |= rg_ge(gm[i], L2) & (0x00010001u << i);
-  return __popc(t);
+  for (int i = 0; i < NG; ++i) {
+    if (i < 16) t0 |= rg_ge(gm[i], L2) & (0x00010001u << i);
+    else t1 |= rg_ge(gm[i], L2) & (0x00010001u << (i - 16));
+  }
+  return __popc(t0) + __popc(t1);
 }
 
 // warp: the largest code t with at least K of the group maxima >= t (0: none)
@@ -273,7 +277,7 @@ __global__ void __launch_bounds__(32 * NW, 1) row_regx_kernel(RgArgs a) {
   constexpr uint32_t B = 128u * CPL, n = B * S;
   constexpr int NBK = 4 * CPL, NS = NBK * KP, NG = 2 * CPL * KP;  // buckets, slots, packed group maxima per lane
   constexpr uint32_t WS = rx_warp_smem<KP, CPL>();
-  static_assert(NG <= 16 && NG <= NW, "group maxima: one folding warp per register");
+  static_assert(NG <= 32 && NS <= 64, "group maxima registers, slots per lane");
   extern __shared__ __align__(128) uint8_t rg_smem[];
   __shared__ uint32_t queue;
   __shared__ volatile uint32_t pred;
@@ -308,16 +312,17 @@ __global__ void __launch_bounds__(32 * NW, 1) row_regx_kernel(RgArgs a) {
         }
       }
     }
-    uint32_t* part = reinterpret_cast<uint32_t*>(wsm);  // [NG][32] per warp, in its staging tile
+    uint32_t* part = reinterpret_cast<uint32_t*>(wsm);  // [NG][32] per warp, from the start of its region
 #pragma unroll
     for (int i = 0; i < NG; ++i) part[i * 32 + lane] = pm[i];
     __syncthreads();
-    uint32_t* res = reinterpret_cast<uint32_t*>(rg_smem + 8 * 256);  // warp 0's state region: [NG][32]
-    if (wid < (uint32_t)NG) {  // warp q folds register q of every warp's share
+    static_assert(2 * NG * 128 <= WS, "partial maxima and the folded result share warp 0's region");
+    uint32_t* res = reinterpret_cast<uint32_t*>(rg_smem + NG * 128);  // behind warp 0's partials: [NG][32]
+    for (uint32_t q = wid; q < (uint32_t)NG; q += NW) {  // a warp folds register q of every warp's share
       uint32_t m = 0xff80ff80u;
       for (uint32_t w2 = 0; w2 < (uint32_t)NW; ++w2)
-        m = bmax_nan(m, reinterpret_cast<const uint32_t*>(rg_smem + (size_t)w2 * WS)[wid * 32 + lane]);
-      res[wid * 32 + lane] = m;
+        m = bmax_nan(m, reinterpret_cast<const uint32_t*>(rg_smem + (size_t)w2 * WS)[q * 32 + lane]);
+      res[q * 32 + lane] = m;
     }
     __syncthreads();
     if (wid == 0) {
@@ -399,20 +404,49 @@ __global__ void __launch_bounds__(32 * NW, 1) row_regx_kernel(RgArgs a) {
       continue;
     }
     const bool posmode = Lkey > 0x8000u;
-    // ---- stage 2: sort the lane's NS slots with the warp's (each bucket's K' already ascending)
-    uint32_t ks[NS];
+    // ---- stage 2: sort the lane's slots with the warp's -----------------------
+    constexpr int NK = NS > 32 ? 32 : NS;  // keys per lane in the sort
+    uint32_t ks[NK];
+    if constexpr (NS <= 32) {  // each bucket's K' slots are already ascending
 #pragma unroll
-    for (int q = 0; q < NS / 4; ++q) {
-      const uint4 sv = reinterpret_cast<const uint4*>(lst)[q];
-      ks[4 * q] = sv.x ^ 0xffff0000u;
-      ks[4 * q + 1] = sv.y ^ 0xffff0000u;
-      ks[4 * q + 2] = sv.z ^ 0xffff0000u;
-      ks[4 * q + 3] = sv.w ^ 0xffff0000u;
+      for (int q = 0; q < NS / 4; ++q) {
+        const uint4 sv = reinterpret_cast<const uint4*>(lst)[q];
+        ks[4 * q] = sv.x ^ 0xffff0000u;
+        ks[4 * q + 1] = sv.y ^ 0xffff0000u;
+        ks[4 * q + 2] = sv.z ^ 0xffff0000u;
+        ks[4 * q + 3] = sv.w ^ 0xffff0000u;
+      }
+      rx_sort<NK, KP>(ks, lane);
+    } else {
+      // 64 slots per lane, ~12 filled: the lane packs its filled slots to the front of its region
+      // (the write index never passes the read index) and sorts 32; a lane with more goes exact
+      uint32_t c = 0;
+#pragma unroll 4
+      for (int q = 0; q < NS; ++q) {
+        const uint32_t e = lst[q];
+        if (e) {
+          lst[c] = e;
+          ++c;
+        }
+      }
+      if (__reduce_max_sync(0xffffffffu, c) > 32u) {
+        __syncwarp();
+        rx_exact<S, KP, CPL>(xr, lane, K, state, ov, oi);
+        continue;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 sv = reinterpret_cast<const uint4*>(lst)[q];
+        ks[4 * q] = (uint32_t)(4 * q) < c ? sv.x ^ 0xffff0000u : 0xffff0000u;
+        ks[4 * q + 1] = (uint32_t)(4 * q + 1) < c ? sv.y ^ 0xffff0000u : 0xffff0000u;
+        ks[4 * q + 2] = (uint32_t)(4 * q + 2) < c ? sv.z ^ 0xffff0000u : 0xffff0000u;
+        ks[4 * q + 3] = (uint32_t)(4 * q + 3) < c ? sv.w ^ 0xffff0000u : 0xffff0000u;
+      }
+      rx_sort<NK, 1>(ks, lane);
     }
-    rx_sort<NS, KP>(ks, lane);
     __syncwarp();
 #pragma unroll
-    for (int q = 0; q < NS / 4; ++q)  // the lane's own region again: element NS lane + i
+    for (int q = 0; q < NK / 4; ++q)  // the lane's own region again: element NK lane + i
       reinterpret_cast<uint4*>(lst)[q] = make_uint4(ks[4 * q], ks[4 * q + 1], ks[4 * q + 2], ks[4 * q + 3]);
     __syncwarp();
     if (posmode && ((~(state[0] >> 16)) & 0x7fffu) > 0x7f80u) nan = 1u;  // a NaN hit sorts first
@@ -421,12 +455,12 @@ __global__ void __launch_bounds__(32 * NW, 1) row_regx_kernel(RgArgs a) {
       __syncwarp();
       continue;
     }
-    for (uint32_t x = lane; x < K; x += 32) {  // sorted element x lives in lane x / NS
-      const uint32_t key = state[(x / NS) * LS + x % NS], code = ~(key >> 16) & 0xffffu;
+    for (uint32_t x = lane; x < K; x += 32) {  // sorted element x lives in lane x / NK
+      const uint32_t key = state[(x / NK) * LS + x % NK], code = ~(key >> 16) & 0xffffu;
       ov[x] = __uint_as_float((posmode ? code : code16_bits(code)) << 16);
       oi[x] = key & 0xffffu;
     }
-    const uint32_t ck = ~(state[((K - 1) / NS) * LS + (K - 1) % NS] >> 16) & 0xffffu;
+    const uint32_t ck = ~(state[((K - 1) / NK) * LS + (K - 1) % NK] >> 16) & 0xffffu;
     const uint32_t Lstar = posmode ? (ck | 0x8000u) : ck;
     if (lane == 0) {
       const uint32_t pv = pred;

@@ -14,7 +14,7 @@ from tests.test_gpu_rowreg import adversarial, bits, u32  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 N = 14336
-CONFIGS = [(2, 512), (4, 256), (8, 128)]
+CONFIGS = [(2, 512), (4, 256), (8, 128), (2, 1024)]
 
 
 def check(ref, cuda, x, kp, B, k):
@@ -37,7 +37,7 @@ def test_rowregx_normal_vs_reference(cuda, ref, kp, B, k):
 
 
 @pytest.mark.parametrize("kp,B", CONFIGS)
-@pytest.mark.parametrize("warps", [16, 28])
+@pytest.mark.parametrize("warps", [16, 28])  # (2, 1024) runs at 16 or 20
 def test_rowregx_adversarial_vs_reference(cuda, ref, opts, kp, B, warps):
     opts("rowregx_warps", warps)
     x = adversarial(N, 287, kp + B)
