@@ -29,6 +29,7 @@ RmPlan plan_rowmax1(int dtype, const void* in, uint64_t rows, uint64_t n, uint64
   const uint64_t S = n / B;
   if (S != 2 && S != 4 && S != 8) return rp;
   if (k > 512 || k > B || reinterpret_cast<uintptr_t>(in) % 8 != 0) return rp;  // the log holds 1024 hits
+  if (rows >= (1ull << 32)) return rp;  // the row list holds 32-bit row indices
   // the exact kernel for the rows left over must take the shape too
   rp.fallback = plan_short(dtype, in, rows, n, B, kp, k, true);
   if (!rp.fallback.ok || reinterpret_cast<uintptr_t>(in) % 16 != 0) return rp;
