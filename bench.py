@@ -336,10 +336,15 @@ class RowsWorkload:
         peak = float(pk["hbm_gbs"])
         alg = self.rows * self.n * self.esz + self.rows * self.b * self.kp * 8
         ach = alg / (kern_ms * 1e-3) / 1e9
+        # SURVEY 8(d)'s end-to-end figure (input + the K outputs) over the whole step, for the kernels that
+        # run stage 1 and stage 2 in one launch and never write the B K' candidates
+        e2e = self.rows * self.n * self.esz + self.rows * self.k * 8
         return {"kernel": self.dominant_kernel(), "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
                 "peak_source": src + " copy bandwidth", "unit": "GB/s", "frac": round(ach / peak, 4),
                 "traffic": traffic_from_profiles(self.args.config), "alg_bytes_per_launch": alg,
-                "launch_ms": round(kern_ms, 5), "share_of_step": round(kern_ms / ms_step, 4)}
+                "launch_ms": round(kern_ms, 5), "share_of_step": round(kern_ms / ms_step, 4),
+                "end_to_end": {"alg_bytes_per_step": e2e, "achieved": round(e2e / (ms_step * 1e-3) / 1e9, 1),
+                               "frac": round(e2e / (ms_step * 1e-3) / 1e9 / peak, 4)}}
 
     def result(self):
         """(values, indices) of the whole batch on this rank (host numpy)."""
