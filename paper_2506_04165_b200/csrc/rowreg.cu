@@ -48,10 +48,13 @@ RgPlan plan_rowreg(int dtype, const void* in, uint64_t rows, uint64_t n, uint64_
   // the unrolled instantiations run best at 28 warps with the loads one tile ahead (72 registers); the
   // run-time row length needs 96 registers to keep its addresses (20 warps: 71 us vs 84 us on the C3 shape)
   const bool unrolled = S == 112 || S == 128 || S == 56 || S == 28;
+  const bool unrolled28 = S == 32 || S == 64 || S == 86 || S == 96 || S == 108;  // 28 warps only
   uint32_t w = (uint32_t)opt("rowreg_warps", 0);
   if (w == 0) {
-    if (!unrolled || opt("rowreg_rt", 0)) {
+    if (opt("rowreg_rt", 0) || (!unrolled && !unrolled28)) {
       w = 20;
+    } else if (unrolled28) {
+      w = 29;
     } else {
       // every warp runs whole rows one after the other and the kernel is issue-bound, so its time goes
       // with waves x warps: the warp count with the fewest idle warp-rows per SM (ties: more warps)
@@ -92,6 +95,12 @@ void run_rowreg(const RgPlan& rp, const void* in, uint64_t rows, uint32_t k, flo
   else if (rp.S == 128 && !rt) rg_dispatch<128>(rp, a, st);
   else if (rp.S == 56 && !rt) rg_dispatch<56>(rp, a, st);
   else if (rp.S == 28 && !rt) rg_dispatch<28>(rp, a, st);
+  // other common FFN widths (4096, 8192, 11008, 12288, 13824): one unrolled instantiation each
+  else if (rp.S == 32 && rp.warps == 29 && !rt) rg_launch<32, 28, 1, 1>(rp, a, st);
+  else if (rp.S == 64 && rp.warps == 29 && !rt) rg_launch<64, 28, 1, 1>(rp, a, st);
+  else if (rp.S == 86 && rp.warps == 29 && !rt) rg_launch<86, 28, 1, 1>(rp, a, st);
+  else if (rp.S == 96 && rp.warps == 29 && !rt) rg_launch<96, 28, 1, 1>(rp, a, st);
+  else if (rp.S == 108 && rp.warps == 29 && !rt) rg_launch<108, 28, 1, 1>(rp, a, st);
   else rg_dispatch<0>(rp, a, st);
   g_prof.bracket_end(st);
 }

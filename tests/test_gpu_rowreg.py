@@ -45,7 +45,8 @@ def check(ref, cuda, x, k):
 
 # n = 128 S: S = 112 is the unrolled instantiation, every other 8 <= S <= 512 takes the run-time row length
 SHAPES = [(14336, 287), (14336, 1), (14336, 512), (14336, 64), (3584, 100), (7168, 287), (16384, 300), (16384, 512),
-          (1024, 40), (1152, 64), (11008, 220), (12800, 300), (28672, 287), (65536, 512), (38400, 100)]
+          (1024, 40), (1152, 64), (11008, 220), (12800, 300), (28672, 287), (65536, 512), (38400, 100),
+          (4096, 82), (8192, 164), (12288, 246), (13824, 276)]
 
 
 @pytest.mark.parametrize("n,k", SHAPES)

@@ -52,7 +52,8 @@ def main():
     with opt("rowreg_rt", 1):
         line("rowreg, run-time row length (S = 0 instantiation)", timeit(run))
     if "--shapes" in sys.argv:  # other row lengths (run-time S) against the previous kernels
-        for n2, k2 in [(3584, 100), (7168, 287), (11008, 220), (16384, 300), (28672, 287), (65536, 512)]:
+        for n2, k2 in [(3584, 100), (4096, 82), (7168, 287), (8192, 164), (11008, 220), (12288, 246), (13824, 276), (16384, 300),
+                       (28672, 287), (65536, 512)]:
             rows2 = max(1024, (235 << 20) // (2 * n2))
             x2 = torch.randn(rows2, n2, device=dev).to(torch.bfloat16)
             out2 = (torch.empty(rows2, k2, device=dev), torch.empty(rows2, k2, dtype=torch.int32, device=dev))
