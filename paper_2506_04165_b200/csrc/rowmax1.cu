@@ -54,7 +54,7 @@ void run_rowmax1(const RmPlan& rp, int dtype, const void* in, uint64_t rows, uin
   a.rows = rows;
   a.CPL = rp.cpl;
   a.k = k;
-  a.margin = (uint32_t)opt("rowreg_margin", 10);
+  a.margin = (uint32_t)opt("rowreg_margin", 12);
   a.force = (uint32_t)opt("rowmax1_force", 0);
   a.out_v = ov;
   a.out_i = oi;
