@@ -82,7 +82,8 @@ void run_rowreg(const RgPlan& rp, const void* in, uint64_t rows, uint32_t k, flo
   a.rows = rows;
   a.S = rp.S;
   a.k = k;
-  a.margin = (uint32_t)opt("rowreg_margin", 12);
+  a.robust = (uint32_t)opt("rowreg_robust", 0);
+  a.margin = (uint32_t)opt("rowreg_margin", 12);  // floor; the kernel widens it by the predictions' tracked spread
   a.force = (uint32_t)opt("rowreg_force", 0);
   a.probe = (uint32_t)opt("rowreg_probe", 0);
   a.out_v = ov;

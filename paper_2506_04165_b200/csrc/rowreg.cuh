@@ -58,6 +58,7 @@ struct RgArgs {
   uint64_t rows;
   uint32_t S;           // stride-rows per bucket (n = 128 S)
   uint32_t k;
+  uint32_t robust;      // 0: per CTA, by the spread of its first rows' scale statistics; 1: always; 2: never
   uint32_t margin;      // prediction: codes below the level of the last row's K-th candidate
   uint32_t force;       // tests: 1 = every row two-pass, 2 = every row exact
   uint32_t probe;       // development: stop after phase `probe`
@@ -146,26 +147,21 @@ __host__ __device__ constexpr int rg_group(int s) {
 // codes, and a NaN raises `nan`.
 template <int S, bool POS, int PF>
 __device__ __forceinline__ void rg_hits(const uint2* p, const uint8_t* nxt, uint32_t L2, uint32_t lane, uint2* stage,
-                                        uint4* state, uint32_t& nan) {
+                                        uint4* state, uint32_t& nan, uint2 (&buf)[2][kRgTile]) {
+  static_assert(PF == 1, "the caller preloads tiles 0 and 1 (the row's scale is read from them)");
   constexpr int NB = (S + kRgTile - 1) / kRgTile;
   constexpr int AH = 3;                    // L2 prefetch distance in tiles (7 x 256 B = 14 lines each)
   constexpr uint32_t TB = kRgTile * 256;   // bytes per tile
   const uint8_t* rowb = reinterpret_cast<const uint8_t*>(p) - 8 * lane;
-  uint2 buf[PF + 1][kRgTile];
-  if (PF) {
-#pragma unroll
-    for (int i = 0; i < kRgTile; ++i)
-      if (i < S) buf[0][i] = rg_ldg(p + i * 32);
-  }
   const uint8_t* col = reinterpret_cast<const uint8_t*>(stage + lane);
   uint4* st4 = state + kRgLaneQ * lane;  // the lane's buckets 4 lane .. 4 lane + 3
 #pragma unroll
   for (int bt = 0; bt < NB; ++bt) {
-    if (bt + PF < NB) {
+    if (bt >= 1 && bt + 1 < NB) {  // tile 1 came with the caller's preload
 #pragma unroll
       for (int i = 0; i < kRgTile; ++i) {
-        const int s = (bt + PF) * kRgTile + i;
-        if (s < S) buf[(bt + PF) % (PF + 1)][i] = rg_ldg(p + s * 32);
+        const int s = (bt + 1) * kRgTile + i;
+        if (s < S) buf[(bt + 1) & 1][i] = rg_ldg(p + s * 32);
       }
     }
     // pull the tile AH ahead into L2 (of this row, then of the warp's next row): the register
@@ -180,7 +176,7 @@ __device__ __forceinline__ void rg_hits(const uint2* p, const uint8_t* nxt, uint
     for (int i = 0; i < kRgTile; ++i) {
       const int s = bt * kRgTile + i;
       if (s < S) {
-        const uint2 v = buf[bt % (PF + 1)][i];
+        const uint2 v = buf[bt & 1][i];
         ax = rg_shl_add(ax, rg_geu1(v.x, L2));
         ay = rg_shl_add(ay, rg_geu1(v.y, L2));
         stage[(6 - i) * 32 + lane] = v;
@@ -243,7 +239,7 @@ __device__ __forceinline__ void rg_max(const uint2* p, uint32_t (&gm)[2][4]) {
 // buffers, the ragged last tile with per-stride-row checks.
 template <bool POS>
 __device__ __forceinline__ void rg_hits_rt(const uint2* p, const uint8_t* nxt, int S, uint32_t L2, uint32_t lane,
-                                           uint2* stage, uint4* state, uint32_t& nan) {
+                                           uint2* stage, uint4* state, uint32_t& nan, uint2 (&pre)[2][kRgTile]) {
   constexpr int AH = 3;
   constexpr uint32_t TB = kRgTile * 256;
   const int NB = (S + kRgTile - 1) / kRgTile;
@@ -307,11 +303,11 @@ __device__ __forceinline__ void rg_hits_rt(const uint2* p, const uint8_t* nxt, i
       }
     }
   };
-  uint2 b0[kRgTile], b1[kRgTile];
-  load(b0, 0);
+  uint2 (&b0)[kRgTile] = pre[0];  // tiles 0 and 1 came with the caller's preload
+  uint2 (&b1)[kRgTile] = pre[1];
 #pragma unroll 1
   for (int bt = 0; bt < NB; bt += 2) {
-    if (bt + 1 < NB) load(b1, bt + 1);
+    if (bt >= 2 && bt + 1 < NB) load(b1, bt + 1);
     process(b0, bt);
     if (bt + 1 < NB) {
       if (bt + 2 < NB) load(b0, bt + 2);
@@ -392,15 +388,102 @@ static __device__ __noinline__ void rg_exact(const uint16_t* xr, int S, uint32_t
 
 template <int S, bool POS, int PF>
 __device__ __forceinline__ void rg_hits_any(const uint2* p, const uint8_t* nxt, int Sx, uint32_t L2, uint32_t lane,
-                                            uint2* stage, uint4* state, uint32_t& nan) {
-  if constexpr (S != 0) rg_hits<S, POS, PF>(p, nxt, L2, lane, stage, state, nan);
-  else rg_hits_rt<POS>(p, nxt, Sx, L2, lane, stage, state, nan);
+                                            uint2* stage, uint4* state, uint32_t& nan, uint2 (&pre)[2][kRgTile]) {
+  if constexpr (S != 0) rg_hits<S, POS, PF>(p, nxt, L2, lane, stage, state, nan, pre);
+  else rg_hits_rt<POS>(p, nxt, Sx, L2, lane, stage, state, nan, pre);
 }
 
 // S = stride-rows (n = 128 S <= 65536; 0 = a run-time argument), B = 128, K' = 4.  CPS CTAs of NW warps per SM;
 // CTA c owns the rows [rows c / G, rows (c + 1) / G) and its warps pull them
 // from a shared counter.  `pred` is the CTA's prediction (an ascending code;
 // ~0 = none).
+// The row's first two tiles (14 stride-rows), loaded ahead of the hit pass:
+// the pass consumes them as its tiles 0 and 1, and rg_row_scale reads the
+// row's scale from them.
+template <int S>
+__device__ __forceinline__ void rg_preload(const uint2* p, int Sx, uint2 (&pre)[2][kRgTile]) {
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int i = 0; i < kRgTile; ++i) {
+      const int s = t * kRgTile + i;
+      if (S != 0 ? s < S : s < Sx) pre[t][i] = rg_ldg(p + s * 32);
+      else pre[t][i] = make_uint2(0xff80ff80u, 0xff80ff80u);
+    }
+}
+// Scale statistic of a row: the mean of 128 log2 (= bf16 codes per octave) of
+// the buckets' largest magnitudes over the first 14 stride-rows, x 16.  A row
+// scaled by s moves it (and a positive K-th candidate level, in the same
+// unit) by 128 log2 s; over i.i.d. normal rows it has sigma ~3.9 codes (the
+// signed maximum has ~19: a bucket whose samples are all small or negative
+// moves the mean by hundreds of codes).  Buckets holding an infinity (masked
+// columns), a NaN or a subnormal do not count.  kRgNoScale = no bucket qualifies.
+constexpr int kRgNoScale = 0x7fffffff;
+// max(|a|, |b|) per half (the sign of the result is not used); NaN wins
+__device__ __forceinline__ uint32_t rg_amax(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.NaN.xorsign.abs.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ int rg_row_scale(const uint2 (&pre)[2][kRgTile]) {
+  uint32_t mx = pre[0][0].x, my = pre[0][0].y;
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int i = 0; i < kRgTile; ++i) {
+      if (t == 0 && i == 0) continue;
+      mx = rg_amax(mx, pre[t][i].x);
+      my = rg_amax(my, pre[t][i].y);
+    }
+  mx &= 0x7fff7fffu;
+  my &= 0x7fff7fffu;
+  const uint32_t c[4] = {mx & 0xffffu, mx >> 16, my & 0xffffu, my >> 16};
+  float sum = 0.f;
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int h = 0; h < 4; ++h)
+    if (c[h] < 0x7f80u && c[h] >= 0x0080u) {  // finite and normal
+      sum += __log2f(__uint_as_float(c[h] << 16));
+      cnt += 1u;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if (cnt == 0u) return kRgNoScale;
+  return __float2int_rn(__fdividef(sum * 2048.f, (float)cnt));
+}
+// a positive level's ascending code <-> 128 log2(value) x 16 (bf16 codes are piecewise linear in
+// the logarithm: up to 11 codes off, which a row's scale would otherwise move in and out of)
+__device__ __forceinline__ int rg_level_log(uint32_t code) {
+  return __float2int_rn(__log2f(__uint_as_float((code & 0x7fffu) << 16)) * 2048.f);
+}
+__device__ __forceinline__ uint32_t rg_log_level(int l16) {  // rounds down
+  const float v = exp2f((float)l16 * (1.f / 2048.f));
+  return min(max(__float_as_uint(v) >> 16, 0x0080u), 0x7f7fu) | 0x8000u;
+}
+
+// Two predictions of a row's K-th candidate level, each with the spread it
+// has shown over the CTA's rows so far: the running mean of the previous
+// rows' levels (precise while the rows keep their scale: sigma ~2-3 codes on
+// i.i.d. rows) and the row's own scale statistic plus the mean offset between
+// level and statistic (sigma ~4.5 codes whatever the rows' scales do).  A row
+// passes against the one with the smaller sigma, kRgSigmas of them below it
+// (never less than the margin argument); an outlier row by the statistic
+// takes the second.  The spreads are sums over the CTA's rows (the warps run
+// in step, so a last-writer running value would see one update per 28 rows),
+// started from the prologue's estimates as kRgPriorRows pseudo-rows and
+// halved every kRgWindow rows.  Levels and offsets are summed relative to the
+// first row's (float sums of small numbers), in codes.
+constexpr float kRgSigmas = 5.2f;
+constexpr float kRgLevelVar = 5.3f;   // codes^2: spread of the K-th level over i.i.d. rows (sigma 2.3)
+constexpr float kRgStatVar = 15.f;    // codes^2: sampling noise of the scale statistic (sigma 3.9)
+constexpr float kRgStableVar = 13.f;  // codes^2: 3 sigma of that variance's estimate over 28 rows
+constexpr float kRgPriorRows = 8.f;
+constexpr uint32_t kRgWindow = 512;
+constexpr float kRgOutlier = 20.f;    // codes: statistic and running mean disagree
+constexpr int kRgOffStep = 64 << 4;   // codes x 16: a row's offset counts within this of the first row's
+constexpr int kRgLevStep = 127 << 4;  // and its level within this (the sums of squares stay below 2^32)
+
 template <int S, int NW, int PF, int CPS>
 __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
   const int Sx = S ? S : (int)a.S;  // S = 0: the row length is a run-time argument
@@ -408,6 +491,43 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
   extern __shared__ __align__(128) uint8_t rg_smem[];
   __shared__ uint32_t queue;
   __shared__ volatile uint32_t pred;
+  // the predictions' statistics (see kRgSigmas); tracked = the prologue produced the references
+  __shared__ volatile uint32_t tracked;
+  // rows of one scale (the statistic's spread over the warps' first rows is its sampling noise) pass
+  // against the running mean alone and skip the statistic; the first failed prediction ends that
+  __shared__ volatile uint32_t robust;
+  __shared__ volatile int ref_l, ref_o;        // the first row's level (code x 16) and log level - statistic
+  __shared__ volatile float var_l0, var_o0;    // prior variances, codes^2
+  // rows, sum and sum of squares of (level - ref_l) and (log level - statistic - ref_o), x 16 and x 256:
+  // integers, so that the updates are plain shared-memory adds (a float add is a compare-and-swap loop)
+  __shared__ volatile uint32_t acc_n, acc_l2, acc_ns, acc_o2;
+  __shared__ volatile int acc_l, acc_o;
+  // what the rows read, refreshed from the sums every fourth row: the two margins, which prediction,
+  // the statistic's offset (x 16), the outlier distance (x 16), the sigmas (statistics only)
+  __shared__ volatile uint32_t d_mgp, d_mgo, d_by;
+  __shared__ volatile int d_off;
+  __shared__ volatile float d_out, d_sgp, d_sgo;
+  auto derive = [&]() {
+    const float n = (float)acc_n, sl = (float)acc_l * (1.f / 16.f), sl2 = (float)acc_l2 * (1.f / 256.f);
+    const float ns = (float)acc_ns, so = (float)acc_o * (1.f / 16.f), so2 = (float)acc_o2 * (1.f / 256.f);
+    const float var_l = (kRgPriorRows * var_l0 + fmaxf(sl2 - sl * sl * __frcp_rn(fmaxf(n, 1.f)), 0.f)) *
+                        __frcp_rn(kRgPriorRows + n);
+    const float var_o = (kRgPriorRows * var_o0 + fmaxf(so2 - so * so * __frcp_rn(fmaxf(ns, 1.f)), 0.f)) *
+                        __frcp_rn(kRgPriorRows + ns);
+    const float inv1 = __frcp_rn(1.f + ns);        // the first row's offset is one sample of the mean
+    const float sg_p = sqrtf(var_l * 1.07f);       // the running mean itself carries ~a quarter sigma
+    const float sg_o = sqrtf(var_o * (1.f + inv1));
+    if ((threadIdx.x & 31) == 0) {
+      d_mgp = max(a.margin, (uint32_t)fminf(ceilf(kRgSigmas * sg_p), 4096.f));
+      d_mgo = max(a.margin, (uint32_t)fminf(ceilf(kRgSigmas * sg_o), 4096.f));
+      d_by = sg_p <= sg_o ? 1u : 0u;
+      d_off = ref_o + (int)(16.f * so * inv1);
+      d_out = 16.f * fmaxf(kRgOutlier, 4.f * sg_o);
+      d_sgp = sg_p;
+      d_sgo = sg_o;
+    }
+  };
+  __shared__ int scale0[32];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t K = a.k;
   uint8_t* wsm = rg_smem + (size_t)wid * kRgWarpSmem;
@@ -419,6 +539,10 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
   if (threadIdx.x == 0) {
     queue = 0;
     pred = 0xffffffffu;
+    tracked = 0;
+    robust = 0;
+    acc_n = acc_l2 = acc_ns = acc_o2 = 0;
+    acc_l = acc_o = 0;
   }
   // ---- prologue: the first prediction from the CTA's first row.  Every warp
   // takes a share of its stride-rows (one DRAM round trip for the CTA instead
@@ -427,6 +551,12 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
   // maximum).  A NaN or -inf-heavy first row leaves no prediction.
   if (a.force == 0) {
     const uint2* p0 = reinterpret_cast<const uint2*>(a.in + r0 * n) + lane;
+    // the scale statistic of the warps' first rows: row r0's pairs with the prediction, their spread
+    // tells whether the rows keep their scale.  Loaded first, so that it shares the round trip of
+    // the warp's share of row r0.
+    uint2 pre0[2][kRgTile];
+    rg_preload<S>(reinterpret_cast<const uint2*>(a.in + (r0 + min((uint32_t)wid, nrows ? nrows - 1 : 0u)) * n) + lane, Sx,
+                  pre0);
     uint32_t pm[2][4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
@@ -437,6 +567,10 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
         pm[0][g] = bmax_nan(pm[0][g], v.x);
         pm[1][g] = bmax_nan(pm[1][g], v.y);
       }
+    }
+    {
+      const int c0 = rg_row_scale(pre0);
+      if (lane == 0) scale0[wid] = c0;
     }
     uint32_t* part = reinterpret_cast<uint32_t*>(wsm);  // [8][32] per warp, in its staging tile
 #pragma unroll
@@ -465,7 +599,28 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
         const uint32_t cg = __reduce_add_sync(0xffffffffu, rg_count_ge(gm0, rg_bits2(t)));
         if (cg >= K) cur = t;
       }
-      if (cur > kRgKeyNegInf && lane == 0) pred = cur << 4;
+      const bool in = lane < (uint32_t)NW;
+      const int c = in ? scale0[lane] : 0;
+      // tracked only for positive levels (a negative level moves against the rows' scale)
+      const bool stat = !__any_sync(0xffffffffu, in && c == kRgNoScale) && cur > 0x8080u;
+      const int mean = (int)__reduce_add_sync(0xffffffffu, c) / NW;
+      const int mad = (int)__reduce_add_sync(0xffffffffu, in ? abs(c - mean) : 0) / NW;
+      if (cur > kRgKeyNegInf && lane == 0) {
+        // the spread of the statistic over the warps' first rows, less its sampling noise, is the
+        // rows' scale spread: it widens the running mean's expected error
+        if (stat) {
+          const float sc = (float)mad * (1.f / (0.8f * 16.f));
+          ref_l = (int)(cur << 4);
+          ref_o = rg_level_log(cur) - scale0[0];
+          var_l0 = kRgLevelVar + fmaxf(sc * sc - kRgStatVar - 4.f, 0.f);  // less a sigma of the estimate
+          var_o0 = kRgLevelVar + kRgStatVar;
+          tracked = 1;
+          robust = (a.robust == 1 || (a.robust == 0 && sc * sc - kRgStatVar > kRgStableVar)) ? 1u : 0u;
+        }
+        pred = cur << 4;
+      }
+      __syncwarp();
+      if (tracked) derive();
     }
   }
   __syncthreads();
@@ -505,13 +660,36 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
     };
     const uint32_t pr = pred;  // running mean of the rows' K-th candidate levels, x 16
     const bool have = pr != 0xffffffffu && a.force == 0;
-    uint32_t Lkey = max(pr >> 4, kRgKeyNegInf + 1 + a.margin) - a.margin;
+    uint2 pre[2][kRgTile];
+    rg_preload<S>(p, Sx, pre);
+    // the level to pass against (see kRgSigmas)
+    const bool trk = tracked != 0;
+    const bool rb = trk && robust != 0;
+    const int crow = rb ? rg_row_scale(pre) : kRgNoScale;
+    bool by_pred = true, both = false;
+    uint32_t mg = a.margin, mg_o = 0;
+    int est = 0;  // the statistic's prediction, log level x 16
+    if (trk) {
+      mg = d_mgp;
+      if (crow != kRgNoScale) {
+        est = crow + d_off;
+        mg_o = d_mgo;
+        by_pred = d_by != 0;
+        // rows that keep their scale, but this row's statistic says otherwise: the lower of the two
+        both = by_pred && fabsf((float)((int)(rg_log_level(est) << 4) - (int)pr)) > d_out;
+      }
+    }
+    uint32_t Lkey = max(pr >> 4, kRgKeyNegInf + 1 + mg) - mg;
+    if (!by_pred || both) {
+      const uint32_t Lo = rg_log_level(est - 16 * (int)mg_o);
+      Lkey = by_pred ? min(Lkey, Lo) : Lo;
+    }
     bool posmode = Lkey > 0x8000u;
     uint32_t M = 0, nan = 0;
     if (have) {
       clear_state();
-      if (posmode) rg_hits_any<S, true, PF>(p, nxt, Sx, rg_bits2(Lkey), lane, stage, state, nan);
-      else rg_hits_any<S, false, PF>(p, nxt, Sx, rg_bits2(Lkey), lane, stage, state, nan);
+      if (posmode) rg_hits_any<S, true, PF>(p, nxt, Sx, rg_bits2(Lkey), lane, stage, state, nan, pre);
+      else rg_hits_any<S, false, PF>(p, nxt, Sx, rg_bits2(Lkey), lane, stage, state, nan, pre);
       M = filled();
     }
     if (a.probe == 1) {  // development: the pass alone (its results consumed)
@@ -521,6 +699,7 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
     bool exact = a.force == 2;
     const bool twopass = M < K;
     if (twopass) {
+      if (have && trk && a.robust != 2 && lane == 0) robust = 1;
       // ---- no usable prediction: the group maxima, the exact K-th largest of
       //      them (it guarantees M >= K), then the hit pass against it
       uint32_t gm[2][4];
@@ -550,8 +729,9 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
       } else {
         posmode = Lkey > 0x8000u;
         clear_state();
-        if (posmode) rg_hits_any<S, true, PF>(p, nxt, Sx, rg_bits2(Lkey), lane, stage, state, nan);
-        else rg_hits_any<S, false, PF>(p, nxt, Sx, rg_bits2(Lkey), lane, stage, state, nan);
+        rg_preload<S>(p, Sx, pre);
+        if (posmode) rg_hits_any<S, true, PF>(p, nxt, Sx, rg_bits2(Lkey), lane, stage, state, nan, pre);
+        else rg_hits_any<S, false, PF>(p, nxt, Sx, rg_bits2(Lkey), lane, stage, state, nan, pre);
         M = filled();
       }
     }
@@ -637,6 +817,11 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
         if (lane == 0) {
           atomicAdd(a.out_i, twopass ? 1u : 0u);
           atomicAdd(a.out_i + 1, M);
+          atomicAdd(a.out_i + 2, by_pred ? 1u : 0u);
+          atomicAdd(a.out_i + 3, by_pred ? mg : mg_o);
+          atomicAdd(a.out_i + 4, (uint32_t)(16.f * d_sgp));
+          atomicAdd(a.out_i + 5, (uint32_t)(16.f * d_sgo));
+          atomicAdd(a.out_i + 6, rb ? 1u : 0u);
         }
       } else {
         for (uint32_t x = lane; x < K; x += 32) {
@@ -651,9 +836,31 @@ __global__ void __launch_bounds__(32 * NW, CPS) row_reg_kernel(RgArgs a) {
     // the next rows' prediction (a racing update by another warp is as good)
     if (lane == 0) {
       const uint32_t pv = pred;
-      pred = pv == 0xffffffffu ? Lstar << 4 : (uint32_t)((int)pv + (((int)(Lstar << 4) - (int)pv) >> 2));
+      const int ls = (int)(Lstar << 4);
+      pred = pv == 0xffffffffu ? (uint32_t)ls : (uint32_t)((int)pv + ((ls - (int)pv) >> 2));
+      if (rb) {
+        const int dl = min(max(ls - ref_l, -kRgLevStep), kRgLevStep);
+        atomicAdd(const_cast<int*>(&acc_l), dl);
+        atomicAdd(const_cast<uint32_t*>(&acc_l2), (uint32_t)(dl * dl));
+        atomicAdd(const_cast<uint32_t*>(&acc_n), 1u);
+        if (crow != kRgNoScale && Lstar > 0x8080u) {
+          const int dn = min(max(rg_level_log(Lstar) - crow - ref_o, -kRgOffStep), kRgOffStep);
+          atomicAdd(const_cast<int*>(&acc_o), dn);
+          atomicAdd(const_cast<uint32_t*>(&acc_o2), (uint32_t)(dn * dn));
+          atomicAdd(const_cast<uint32_t*>(&acc_ns), 1u);
+        }
+        if (acc_n >= kRgWindow) {  // forget: racing updates lose a row or two
+          acc_n = acc_n >> 1;
+          acc_l = acc_l / 2;
+          acc_l2 = acc_l2 >> 1;
+          acc_ns = acc_ns >> 1;
+          acc_o = acc_o / 2;
+          acc_o2 = acc_o2 >> 1;
+        }
+      }
     }
     __syncwarp();
+    if (rb && (acc_n & 3u) == 0u) derive();
   }
 }
 

@@ -131,6 +131,43 @@ def test_rowreg_scale_changes(cuda, ref):
     check(ref, cuda, x, 287)
 
 
+@pytest.mark.parametrize("robust", [0, 1, 2])
+@pytest.mark.parametrize("kind", ["spread", "drift", "negative", "masked", "spikes", "sparse", "halves"])
+@pytest.mark.parametrize("n,k", [(14336, 287), (12288, 246)])
+def test_rowreg_row_scales(cuda, ref, opts, robust, kind, n, k):
+    """Rows of different scales, with the scale-statistic prediction always on
+    (1), chosen per CTA (0) and off (2): the level a row passes against only
+    steers speed.  spread: scale 2^U(-3,3) per row; drift: scale growing along
+    the batch; negative: every value below zero (the level moves against the
+    scale); masked: -inf columns (no statistic from them); spikes: a few huge
+    magnitudes per row; sparse: mostly zeros (subnormal-free statistic over
+    few buckets); halves: two populations of rows."""
+    opts("rowreg_robust", robust)
+    rng = np.random.default_rng(len(kind) * 131 + robust + n)
+    rows = 1800
+    x = rng.standard_normal((rows, n)).astype(np.float32)
+    if kind == "spread":
+        x *= np.exp2(rng.uniform(-3, 3, size=(rows, 1))).astype(np.float32)
+    elif kind == "drift":
+        x *= np.exp2(np.linspace(-2, 2, rows))[:, None].astype(np.float32)
+    elif kind == "negative":
+        x = -np.abs(x) * np.exp2(rng.uniform(-2, 2, size=(rows, 1))).astype(np.float32) - 0.01
+    elif kind == "masked":
+        x *= np.exp2(rng.uniform(-1, 1, size=(rows, 1))).astype(np.float32)
+        x[:, rng.choice(n, size=n // 3, replace=False)] = -np.inf
+        x[::5, : n // 2] = -np.inf
+        x[7] = -np.inf
+    elif kind == "spikes":
+        for r in range(rows):
+            x[r, rng.integers(0, n, size=6)] *= 1e4
+    elif kind == "sparse":
+        x *= (rng.random((rows, n)) < 0.05)
+    elif kind == "halves":
+        x[rows // 2:] *= 37.0
+        x[::2] *= 0.6
+    check(ref, cuda, x, k)
+
+
 def test_rowreg_nan_raises(cuda):
     x = np.random.default_rng(3).standard_normal((600, 14336)).astype(np.float32)
     x[457, 777] = np.nan
