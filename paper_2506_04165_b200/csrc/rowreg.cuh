@@ -8,30 +8,32 @@
 //   * lane l reads its own 8 bytes (buckets 4l..4l+3, topk.hpp:13-15: element
 //     i goes to bucket i mod B) of every stride-row straight into registers
 //     (256 B per warp load, 16 loads in flight per lane, double-buffered);
-//   * per bf16x2 word one packed 3-input max (the group maxima, two words
-//     per instruction) and one packed compare + mask-or (the hit map): no
-//     branch, no per-bucket state in the loop;
-//   * every 16 stride-rows the lane walks the set bits of its hit map and
-//     copies the hits (value | position) from its own column of the staging
-//     tile to its log -- the row is never read again.
+//   * per bf16x2 word one packed compare against the level (set.geu) and one
+//     packed a*2 + hit (fma.rn.bf16x2): after a tile of 7 stride-rows each
+//     half holds 128 + its 7 hit bits; no branch, no per-bucket state in the
+//     loop;
+//   * after every tile the lane walks the set bits and inserts the hits
+//     (code << 16 | position, read back from its own column of the staging
+//     tile) into the bucket's 4-slot state in Alg. 1 order (topk.cpp:80-102)
+//     -- the row is never read again.
 // Threshold argument: for a level L let c_b = the elements of
 // bucket b that are >= L and M = sum_b min(K', c_b).  If M >= K the top K of
 // the row's candidates are the top K of its candidates >= L, and those
 // follow from the elements >= L alone (Alg. 1 over a bucket's elements >= L,
-// topk.cpp:80-102, the S* lemma).  M is known exactly after the pass (the
-// popcounts of the hit map), so ANY level may be tried:
-//   fast path   L0 = the CTA's prediction: the level of the K-th candidate of
-//               the row finished last (a by-product of its stage 2) minus a
-//               margin.  One pass; M >= K afterwards proves it.
-//   two-pass    no prediction yet, M < K, or a lane's log overflowed: the
-//               exact K-th largest of the B K' group maxima (K' disjoint groups
-//               of stride-rows per bucket; 16 packed-compare rounds on the
-//               maxima the first pass kept) guarantees M >= K; a second pass
-//               (the row is in L2) logs the hits against it.
-//   exact path  L = -inf, or a log overflows even then (ties at L, one
-//               bucket holding the large values): Alg. 1 of every bucket as
-//               the reference runs it, then a bitonic sort of the B K' rank
-//               keys.  Slow; degenerate rows only.
+// the S* lemma).  M is known exactly after the pass (the filled slots), so
+// ANY level may be tried:
+//   fast path   the CTA's prediction of the level of the row's K-th
+//               candidate minus a margin: the running mean of the previous
+//               rows' levels, or -- when the rows' scales differ -- the
+//               row's own scale statistic plus the mean offset (kRgSigmas
+//               below).  One pass; M >= K afterwards proves it.
+//   two-pass    no prediction yet or M < K: the exact K-th largest of the
+//               B K' group maxima (K' disjoint groups of stride-rows per
+//               bucket) guarantees M >= K; a second pass (the row is in L2)
+//               inserts the hits against it.
+//   exact path  L = -inf: Alg. 1 of every bucket as the reference runs it,
+//               then a bitonic sort of the B K' rank keys.  Slow; degenerate
+//               rows only.
 // After the pass the states hold the row's candidates >= L; a bitonic sort
 // of the 512 slots in registers writes the first K in output order
 // (topk.cpp:30-50).
